@@ -1,0 +1,450 @@
+"""Benchmark: GPU0->GPU1 multi-path transfer bandwidth (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N = 1 (the driver's default): one visible B200, so the transfer runs in
+loopback — logical GPU0 and GPU1 of the topology both map to cuda:0.  The
+direct path is then an HBM->HBM copy by the SM transfer kernel and the
+host-staged path a real D2H + H2D over PCIe Gen5 through pinned memory; the
+planner, graph cache and engine are exactly the multi-GPU ones.
+A step = one message of --size bytes (default 512 MiB, larger than L2, so no
+L2 flush is needed) sent with the cached CUDA graph.  `value` is S*K / device
+time of K steps; `e2e` adds the H2D of the source from pinned host memory
+and the D2H of the delivered buffer to every step, through the public API.
+
+--impl reference: the reference's CPU implementation of the path — the
+oracle restatement (oracle/transfer.py, the reference package itself never
+moves bytes) — timed on the host cores on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MiB = 1 << 20
+METRIC = "GPU0→GPU1 bandwidth GB/s vs msg size (1KB–512MB), multi-path vs single-path"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--size", type=int, default=512 * MiB)
+    ap.add_argument("--chunks", type=int, default=8)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--window", type=int, default=16)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return d.get("hbm_gbs", 6650.0), "measured"
+    except OSError:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=6)
+
+    def summary(self):
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0)),
+            "model": model}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the CPU implementation of the path (oracle port)
+# ---------------------------------------------------------------------------
+def cpu_transfer_rate(size, chunks, budget_s, threads, kinds_shares=None):
+    """Bytes/s of the oracle's host-memory multi-path transfer (planner + copies)."""
+    import numpy as np
+
+    from oracle import planner as op
+    from oracle import transfer as ot
+    topo = op.parse_topology(loopback_topo_text(3000e9, 50e9))
+    paths = op.plan_paths(topo, 0, 1, 1, True)
+    src = ot.pattern(size)
+    dst = np.empty_like(src)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        plan = op.make_chunk_plan([p["share"] for p in paths], size, chunks)
+        ot.run(src, dst, [p["kind"] for p in paths], plan, threads=threads)
+        n += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    assert np.array_equal(src, dst)
+    return n * size / dt, n
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    size = args.size
+    # warm-up then K timed steps, each one message through the CPU path
+    import numpy as np
+
+    from oracle import planner as op
+    from oracle import transfer as ot
+    topo = op.parse_topology(loopback_topo_text(3000e9, 50e9))
+    paths = op.plan_paths(topo, 0, 1, 1, True)
+    src = ot.pattern(size)
+    dst = np.empty_like(src)
+    for _ in range(args.warmup):
+        plan = op.make_chunk_plan([p["share"] for p in paths], size, args.chunks)
+        ot.run(src, dst, [p["kind"] for p in paths], plan, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        plan = op.make_chunk_plan([p["share"] for p in paths], size, args.chunks)
+        ot.run(src, dst, [p["kind"] for p in paths], plan, threads=threads)
+    dt = time.perf_counter() - t0
+    assert np.array_equal(src, dst)
+    gbs = args.steps * size / dt / 1e9
+    sample = f"{args.steps} x {size} B messages, direct+host plan, {threads} threads, numpy"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": sample, **cpu_info()},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def loopback_topo_text(link_bw, host_bw, n=2):
+    from paper_2604_22228_b200 import mesh_text
+    return mesh_text("b200_loopback", n, link_bw, 1, 2e-6, host_bw, 10e-6, "full")
+
+
+def workload_config(args):
+    return {"workload": f"osu_bw-style GPU0->GPU1, {args.size} B messages, direct + host-staged "
+                        f"multi-path, max_chunks {args.chunks}, cached CUDA-graph replay; N=1: "
+                        "logical GPU0/GPU1 both on cuda:0 (loopback: direct = HBM copy, "
+                        "host = PCIe Gen5 D2H+H2D)",
+            "msg_bytes": args.size, "max_chunks": args.chunks, "paths": "direct+host",
+            "l2": "inputs larger than L2 (512 MiB > 126 MB)", "parallelism": f"n{args.gpus}"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def time_sends(torch, eng, cfg, src, dst, size, steps, warmup, stream, window=1):
+    for _ in range(warmup):
+        eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps * window):
+        eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / (steps * window)
+
+
+def run_ours(args, rank, world):
+    import torch
+
+    from paper_2604_22228_b200 import Engine, PathConfig, load_topology
+    dev = rank % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    hbm_peak, peak_kind = peaks()
+
+    # 1. probe per-path bandwidths -> reference-schema .topo (SURVEY §8c protocol)
+    probe = Engine.loopback(2, dev)
+    m = probe.measure_paths(0, 1, 256 * MiB, 5)
+    probe.close()
+    link_bw = max(m["direct_sm"], m["direct_ce"]) * 1e9
+    host_bw = min(m["d2h"], m["h2d"]) * 1e9
+    topo_text = loopback_topo_text(link_bw, host_bw)
+    eng = Engine(load_topology(topo_text), [dev, dev])
+    size = args.size
+    cfg = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=args.chunks,
+                     graph_mode=True)
+    src = torch.empty(size, dtype=torch.uint8, device=f"cuda:{dev}")
+    dst = torch.empty_like(src)
+    src.copy_(torch.randint(0, 256, (size,), dtype=torch.uint8,
+                            generator=torch.Generator().manual_seed(20261017)).to(src.device))
+    dst.copy_(torch.bitwise_not(src))
+    stream = torch.cuda.Stream(device=dev)
+
+    # correctness of the benchmarked configuration (bytes + plan vs oracle)
+    eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
+    eng.sync()
+    torch.cuda.synchronize()
+    assert torch.equal(src, dst), "delivered bytes differ"
+    from oracle import planner as op
+    opaths = op.plan_paths(op.parse_topology(topo_text), 0, 1, 1, True)
+    ochunks = op.make_chunk_plan([p["share"] for p in opaths], size, args.chunks)
+    _, chunks = eng.last_plan()
+    assert [(c.path_index, c.offset, c.length, c.seq) for c in chunks] == ochunks
+    direct_bytes = sum(c[2] for c in ochunks if c[0] == 0)
+    host_bytes = size - direct_bytes
+
+    # 2. headline: K steps of graph replay, device time, clocks sampled
+    for _ in range(args.warmup):
+        eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(dev) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 1e3
+    st = eng.stats()
+    if world > 1:
+        tt = torch.tensor([t], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt)
+    value = world * args.steps * size / t / 1e9
+
+    # 3. dominant kernel: transfer_kernel duration (events on its stream, streamed mode)
+    cfg_s = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=args.chunks,
+                       graph_mode=False)
+    ktimes = []
+    for _ in range(max(3, args.steps // 2)):
+        eng.send(src, dst, size, cfg_s, stream=stream, src_dev=0, dst_dev=1)
+        ktimes.append(eng.kernel_time_ms())
+    kms = statistics.mean(ktimes[1:])
+    k_alg_bytes = 2 * direct_bytes  # HBM read + write of the direct share
+    achieved = k_alg_bytes / (kms / 1e3) / 1e9
+    path_roofline = hbm_peak / 2 + min(m["d2h"], m["h2d"])
+
+    # 4. e2e through the public API with host buffers
+    hsrc = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+    hdst = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+    hsrc.copy_(src.cpu())
+    e2e_steps = max(3, args.steps // 4)
+    for _ in range(2):
+        src.copy_(hsrc, non_blocking=True)
+        eng.send(src, dst, size, cfg, src_dev=0, dst_dev=1)
+        hdst.copy_(dst, non_blocking=True)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cur = torch.cuda.current_stream()
+    c0.record(cur)
+    for _ in range(e2e_steps):
+        src.copy_(hsrc, non_blocking=True)
+        eng.send(src, dst, size, cfg, src_dev=0, dst_dev=1)
+        hdst.copy_(dst, non_blocking=True)
+    c1.record(cur)
+    torch.cuda.synchronize()
+    e2e = e2e_steps * size / (c0.elapsed_time(c1) / 1e3) / 1e9
+    assert torch.equal(hdst, hsrc)
+
+    # 5. osu_bw-style sweep: single path CE / SM vs multi-path graph on / off
+    sweep = []
+    if not args.no_sweep:
+        sweep = run_sweep(torch, eng, topo_text, dev, stream, args.window)
+
+    # 6. lifecycle (BASELINE config 5) and the reference's CPU path timing
+    lifecycle = run_lifecycle(torch, eng, dev, stream)
+    cpu = None
+    if rank == 0:
+        cpu_rate, nmsg = cpu_transfer_rate(64 * MiB, args.chunks, 10.0,
+                                           len(os.sched_getaffinity(0)))
+        cpu = {"value": cpu_rate / 1e9, "unit": "GB/s", "cores": len(os.sched_getaffinity(0)),
+               "kind": "port", "sample": f"{nmsg} x 64 MiB messages, direct+host plan, "
+                                         "oracle/transfer.py numpy copies, ~10 s", **cpu_info()}
+    if rank != 0:
+        return
+    launches = args.steps * st.kernels
+    out = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (seeded random bytes, seed 20261017)",
+        "config": workload_config(args),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "kernel": "mpk::transfer_kernel<8>", "kernel_ms": kms,
+                     "alg_bytes_per_launch": k_alg_bytes, "peak_kind": peak_kind},
+        "path_roofline": {"R_gbs": path_roofline, "frac": value / path_roofline,
+                          "hbm_copy_gbs": hbm_peak / 2, "pcie_gbs": min(m["d2h"], m["h2d"]),
+                          "probe": m, "direct_bytes": direct_bytes, "host_bytes": host_bytes},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": size,
+                "d2h_bytes_per_step": size},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "graph": {"nodes_logical": st.nodes_logical, "nodes_physical": st.nodes_physical,
+                  "kernels_per_send": st.kernels, "ce_copies_per_send": st.ce_copies,
+                  "launch_us": st.launch_us},
+        "lifecycle": lifecycle,
+        "sweep": sweep,
+    }
+    print(json.dumps(out), flush=True)
+
+
+SWEEP_SIZES = [1 << k for k in range(10, 30)]
+
+
+def run_sweep(torch, eng, topo_text, dev, stream, window):
+    from paper_2604_22228_b200 import Engine, PathConfig, load_topology
+    rows = []
+    ce = Engine(load_topology(topo_text), [dev, dev])
+    ce.configure(direct="ce")
+    single_ce = PathConfig(max_chunks=1, graph_mode=False)
+    single_sm = PathConfig(max_chunks=1, graph_mode=True)
+    multi_g = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=8, graph_mode=True)
+    multi_s = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=8, graph_mode=False)
+    big = torch.empty(SWEEP_SIZES[-1], dtype=torch.uint8, device=f"cuda:{dev}")
+    out = torch.empty_like(big)
+    for size in SWEEP_SIZES:
+        src, dst = big[:size], out[:size]
+        steps = 20 if size > MiB else 100
+        warm = 2 if size > MiB else 10
+        row = {"bytes": size}
+        for name, e, cfg in (("ce_single", ce, single_ce), ("sm_single", eng, single_sm),
+                             ("multi_graph", eng, multi_g), ("multi_stream", eng, multi_s)):
+            s = time_sends(torch, e, cfg, src, dst, size, steps, warm, stream, window=1)
+            row[name] = size / s / 1e9
+        rows.append(row)
+    ce.close()
+    return rows
+
+
+def run_lifecycle(torch, eng, dev, stream):
+    """Capture+instantiate / cached replay / per-call stream launch, host us per message."""
+    from paper_2604_22228_b200 import PathConfig
+    res = []
+    big = torch.empty(4 * MiB, dtype=torch.uint8, device=f"cuda:{dev}")
+    out = torch.empty_like(big)
+    for size in (4 << 10, 16 << 10, 64 << 10, 256 << 10, MiB, 4 * MiB):
+        src, dst = big[:size], out[:size]
+        g = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=1, graph_mode=True)
+        s = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=1, graph_mode=False)
+        row = {"bytes": size}
+        # (a) capture + instantiate every call
+        cap = []
+        for _ in range(20):
+            eng.clear_cache()
+            eng.send(src, dst, size, g, stream=stream, src_dev=0, dst_dev=1)
+            st = eng.stats()
+            cap.append((st.creation_us, st.construction_us, st.instantiation_us, st.launch_us,
+                        st.plan_us))
+        row["capture_every_call_us"] = {
+            "creation": statistics.median(c[0] for c in cap),
+            "construction": statistics.median(c[1] for c in cap),
+            "instantiation": statistics.median(c[2] for c in cap),
+            "launch": statistics.median(c[3] for c in cap),
+            "plan": statistics.median(c[4] for c in cap)}
+        # (b) cached replay, (c) per-call stream launch: host us per message + device latency
+        for name, cfg in (("replay", g), ("stream", s)):
+            for _ in range(10):
+                eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
+            torch.cuda.synchronize()
+            n = 2000
+            t0 = time.perf_counter()
+            for _ in range(n):
+                eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
+            host_us = (time.perf_counter() - t0) / n * 1e6
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            lat = []
+            for _ in range(50):
+                e0.record(stream)
+                eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
+                e1.record(stream)
+                e1.synchronize()
+                lat.append(e0.elapsed_time(e1) * 1e3)
+            row[name] = {"host_us_per_msg": host_us, "gpu_latency_us": statistics.median(lat),
+                         "launch_us": eng.stats().launch_us}
+        row["nodes_logical"] = eng.stats().nodes_logical
+        res.append(row)
+    return res
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if args.impl == "ours":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+        dist.init_process_group(backend)
+    if args.impl == "reference":
+        run_reference(args, rank)
+    else:
+        run_ours(args, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,885 @@
+// mp_engine.cu — the B200 execution engine behind mp_send.
+//
+// Replaces the reference's simulated execution (sim.py:152-292) with real
+// data movement, keeping its semantics:
+//   * the chunk plan is the reference planner's, bit-exact (core.hpp);
+//   * a staged chunk's hop2 starts only after its hop1 finished
+//     (graph.py:115-117, sim.py:182-191) — a device flag for SM lanes, a
+//     CUDA event / graph edge for copy-engine lanes;
+//   * copy-engine lanes are FIFO streams, one per (path, hop)
+//     (pipeline.py:102-125, "two separate CUDA streams");
+//   * graph mode captures the whole multi-path workflow once and replays it
+//     from an LRU cache keyed by (src, dst, size, devices, path set)
+//     (graph.py:121-186).
+//
+// Physical layout of one send on B200:
+//   * every NVLink/HBM path (direct, relay hop1, relay hop2) handled by the SM
+//     engine becomes tiles of ONE persistent transfer kernel per physical
+//     device (mp_kernels.cuh): one launch per device regardless of chunk count;
+//   * copy-engine paths (host-staged always; direct/relay when configured)
+//     become cudaMemcpyAsync on lane streams with per-chunk events;
+//   * fork/join events tie all lanes to the caller's stream.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <list>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "core.hpp"
+#include "mp_kernels.cuh"
+
+using namespace mp;
+
+namespace {
+
+constexpr int kUnroll = 8;
+
+struct CudaError {
+  std::string msg;
+};
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t _e = (call);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      throw Error{MP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)};     \
+  } while (0)
+
+double now_us() {
+  using namespace std::chrono;
+  return duration<double, std::micro>(steady_clock::now().time_since_epoch()).count();
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() { cudaGetDevice(&prev); }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// Physical CUDA device owned by the context.
+struct Phys {
+  int ordinal = 0;
+  int sms = 148;
+  mpk::Ctl* ctl = nullptr;               // transfer-kernel control block
+  cudaStream_t kstream = nullptr;        // SM transfer-kernel stream
+  cudaStream_t capture = nullptr;        // graph-capture origin
+  std::vector<cudaStream_t> lanes;       // copy-engine lane streams
+  std::vector<cudaEvent_t> events;       // handoff / fork / join events
+  size_t next_event = 0;
+  cudaEvent_t kt0 = nullptr, kt1 = nullptr;  // kernel timing
+};
+
+// Logical accelerator (several may map to one physical device: loopback).
+struct Logi {
+  int phys = 0;
+  uint8_t* stage = nullptr;  // relay staging arena
+  size_t stage_cap = 0;
+  uint32_t* flags = nullptr;  // [flag_cap] chunk flags + [flag_cap] pass counters
+  int flag_cap = 0;
+};
+
+struct CeOp {
+  int phys;        // device whose lane stream runs it
+  int lane;        // lane stream index on that device
+  void* dst;
+  const void* src;
+  size_t len;
+  int wait_ev;     // index into the op-event list to wait on, -1 none
+  int record_ev;   // index into the op-event list to record, -1 none
+};
+
+struct Program {
+  int phys;
+  mpk::Tile* d_tiles = nullptr;
+  unsigned ntiles = 0;
+  unsigned grid = 0;
+};
+
+struct Entry {
+  std::string key;
+  std::vector<mp_path> paths;
+  std::vector<mp_chunk> chunks;
+  int nodes_logical = 0;
+  std::vector<Program> progs;
+  std::vector<CeOp> ce;
+  std::vector<int> ev_phys;  // device of each op event
+  int src_phys = 0;
+  cudaGraphExec_t exec = nullptr;
+  int nodes_physical = 0;
+  bool graph = false;
+};
+
+}  // namespace
+
+struct mp_ctx {
+  std::vector<Phys> phys;
+  std::vector<Logi> logi;
+  std::vector<int> peer;  // n_phys x n_phys can-access matrix
+  bool has_topo = false;
+  Topology topo;
+  mp_engine_opts opts{};
+  uint8_t* host_stage = nullptr;
+  size_t host_cap = 0;
+  std::list<Entry*> lru;  // least recent first
+  std::unordered_map<std::string, std::list<Entry*>::iterator> index;
+  mp_send_stats stats{};
+  std::vector<mp_path> last_paths;
+  std::vector<mp_chunk> last_chunks;
+  cudaEvent_t last_done = nullptr;  // serialises sends issued on different streams
+  void* last_stream = nullptr;
+  bool have_last = false;
+  double kernel_ms = 0.0;
+  std::mutex mu;
+};
+
+namespace {
+
+cudaEvent_t take_event(Phys& p) {
+  if (p.next_event >= p.events.size()) {
+    DeviceGuard g;
+    CK(cudaSetDevice(p.ordinal));
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p.events.push_back(e);
+  }
+  return p.events[p.next_event++];
+}
+
+cudaStream_t lane_stream(Phys& p, int lane) {
+  while ((int)p.lanes.size() <= lane) {
+    DeviceGuard g;
+    CK(cudaSetDevice(p.ordinal));
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    p.lanes.push_back(s);
+  }
+  return p.lanes[lane];
+}
+
+void destroy_entry(mp_ctx* ctx, Entry* e) {
+  if (!e) return;
+  for (auto& pr : e->progs) {
+    cudaSetDevice(ctx->phys[pr.phys].ordinal);
+    if (pr.d_tiles) cudaFree(pr.d_tiles);
+  }
+  if (e->exec) cudaGraphExecDestroy(e->exec);
+  delete e;
+}
+
+void clear_cache(mp_ctx* ctx) {
+  for (auto& p : ctx->phys) {
+    cudaSetDevice(p.ordinal);
+    cudaDeviceSynchronize();
+  }
+  for (Entry* e : ctx->lru) destroy_entry(ctx, e);
+  ctx->lru.clear();
+  ctx->index.clear();
+}
+
+// Grow staging arenas; cached programs point into them, so growth drops the cache.
+void ensure_arenas(mp_ctx* ctx, const std::vector<size_t>& stage_need, int flags_need,
+                   size_t host_need) {
+  bool grow = host_need > ctx->host_cap;
+  for (size_t i = 0; i < ctx->logi.size(); ++i)
+    if (stage_need[i] > ctx->logi[i].stage_cap || (stage_need[i] && flags_need > ctx->logi[i].flag_cap))
+      grow = true;
+  if (!grow) return;
+  clear_cache(ctx);
+  DeviceGuard g;
+  for (size_t i = 0; i < ctx->logi.size(); ++i) {
+    Logi& L = ctx->logi[i];
+    if (stage_need[i] == 0) continue;
+    CK(cudaSetDevice(ctx->phys[L.phys].ordinal));
+    if (stage_need[i] > L.stage_cap) {
+      if (L.stage) CK(cudaFree(L.stage));
+      size_t cap = std::max(stage_need[i], (size_t)2 * L.stage_cap);
+      cap = (cap + 4095) & ~(size_t)4095;
+      CK(cudaMalloc(&L.stage, cap));
+      L.stage_cap = cap;
+    }
+    if (flags_need > L.flag_cap) {
+      if (L.flags) CK(cudaFree(L.flags));
+      int cap = std::max(flags_need, 2 * L.flag_cap);
+      CK(cudaMalloc(&L.flags, (size_t)cap * 2 * sizeof(uint32_t)));
+      CK(cudaMemset(L.flags, 0, (size_t)cap * 2 * sizeof(uint32_t)));
+      CK(cudaDeviceSynchronize());
+      L.flag_cap = cap;
+    }
+  }
+  if (host_need > ctx->host_cap) {
+    if (ctx->host_stage) CK(cudaFreeHost(ctx->host_stage));
+    size_t cap = std::max(host_need, (size_t)2 * ctx->host_cap);
+    cap = (cap + 4095) & ~(size_t)4095;
+    CK(cudaHostAlloc((void**)&ctx->host_stage, cap, cudaHostAllocPortable | cudaHostAllocMapped));
+    ctx->host_cap = cap;
+  }
+}
+
+uint64_t auto_tile_bytes(const mp_ctx* ctx, uint64_t path_bytes, int sms) {
+  if (ctx->opts.tile_bytes > 0) return (uint64_t)ctx->opts.tile_bytes;
+  // aim for >= 4 tiles per resident CTA, 16 KiB .. 1 MiB, multiple of 4 KiB
+  uint64_t ctas = (uint64_t)sms * std::max(1, ctx->opts.ctas_per_sm);
+  uint64_t t = path_bytes / (ctas * 4);
+  t = std::max<uint64_t>(t, 16 << 10);
+  t = std::min<uint64_t>(t, 1 << 20);
+  return (t + 4095) & ~(uint64_t)4095;
+}
+
+struct Building {
+  std::vector<std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>> tiles;  // per phys
+};
+
+// Split [src, src+len) -> dst into tiles appended to `out`.
+void append_tiles(std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>& out,
+                  uint64_t order, uint64_t src, uint64_t dst, uint64_t len, uint64_t tile,
+                  const mpk::Tile& proto) {
+  for (uint64_t o = 0; o < len; o += tile) {
+    mpk::Tile t = proto;
+    t.src = src + o;
+    t.dst = dst + o;
+    t.len = std::min(tile, len - o);
+    out.push_back({{order, out.size()}, t});
+  }
+}
+
+uint64_t ntiles_of(uint64_t len, uint64_t tile) { return (len + tile - 1) / tile; }
+
+// Lower a chunk plan to device programs and copy-engine ops.
+Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* dst, uint64_t size,
+                   int src_dev, int dst_dev, const mp_config& cfg) {
+  auto* e = new Entry();
+  e->key = key;
+  e->paths = plan_paths(ctx->topo, src_dev, dst_dev, cfg);
+  e->chunks = make_chunk_plan(e->paths.data(), (int)e->paths.size(), (int64_t)size, cfg.max_chunks);
+  const int np = (int)e->paths.size();
+  const int nc = (int)e->chunks.size();
+  for (const mp_chunk& c : e->chunks) e->nodes_logical += e->paths[c.path_index].nhops;
+  const mp_engine_opts& o = ctx->opts;
+  const int sp = ctx->logi[src_dev].phys, dp = ctx->logi[dst_dev].phys;
+  e->src_phys = sp;
+
+  // per-path byte totals and nominal lengths
+  std::vector<uint64_t> path_bytes(np, 0), nominal(np, 0);
+  std::vector<int> path_count(np, 0);
+  for (const mp_chunk& c : e->chunks) {
+    path_bytes[c.path_index] += c.length;
+    nominal[c.path_index] = std::max<uint64_t>(nominal[c.path_index], c.length);
+    path_count[c.path_index] += 1;
+  }
+  // staging requirements
+  std::vector<size_t> stage_need(ctx->logi.size(), 0);
+  size_t host_need = 0;
+  int host_slots = 0;
+  for (int p = 0; p < np; ++p) {
+    if (e->paths[p].kind == MP_PATH_GPU) stage_need[e->paths[p].stage] = path_bytes[p];
+    if (e->paths[p].kind == MP_PATH_HOST) {
+      host_slots = o.host_slots > 0 ? std::min(o.host_slots, path_count[p]) : path_count[p];
+      host_need = host_slots < path_count[p] ? (size_t)host_slots * nominal[p] : path_bytes[p];
+    }
+  }
+  ensure_arenas(ctx, stage_need, nc, host_need);
+
+  const uint64_t s0 = (uint64_t)(uintptr_t)src, d0 = (uint64_t)(uintptr_t)dst;
+  std::vector<std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>> tiles(ctx->phys.size());
+  std::vector<uint64_t> stage_off(np, 0);
+  std::vector<int> lane_base(np, 0);
+  {
+    int l = 0;
+    for (int p = 0; p < np; ++p) {
+      lane_base[p] = l;
+      l += e->paths[p].nhops;
+    }
+  }
+  std::vector<int> hop2_done_ev(nc, -1);  // host WAR: event recorded after hop2 of chunk
+  std::vector<int> host_chunk_of_seq;
+  auto new_event = [&](int phys) {
+    e->ev_phys.push_back(phys);
+    return (int)e->ev_phys.size() - 1;
+  };
+
+  for (int c = 0; c < nc; ++c) {
+    const mp_chunk& ch = e->chunks[c];
+    const mp_path& P = e->paths[ch.path_index];
+    const int p = ch.path_index;
+    const uint64_t round = (uint64_t)ch.seq;
+    if (P.kind == MP_PATH_DIRECT) {
+      const bool sm = o.direct_engine == MP_ENGINE_SM && size >= (uint64_t)o.sm_min_bytes;
+      if (sm) {
+        int exec = o.pull ? dp : sp;
+        mpk::Tile proto{};
+        uint64_t tile = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[exec].sms);
+        append_tiles(tiles[exec], 2 * round, s0 + ch.offset, d0 + ch.offset, ch.length, tile, proto);
+      } else {
+        e->ce.push_back(CeOp{sp, lane_base[p], (uint8_t*)dst + ch.offset, (const uint8_t*)src + ch.offset,
+                             (size_t)ch.length, -1, -1});
+      }
+    } else if (P.kind == MP_PATH_GPU) {
+      Logi& L = ctx->logi[P.stage];
+      const int rp = L.phys;
+      uint8_t* stage = L.stage + stage_off[p];
+      stage_off[p] += ch.length;
+      const bool sm = o.relay_engine == MP_ENGINE_SM && size >= (uint64_t)o.sm_min_bytes;
+      if (sm) {
+        uint64_t t1 = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[sp].sms);
+        uint64_t t2 = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[rp].sms);
+        uint32_t n1 = (uint32_t)ntiles_of(ch.length, t1), n2 = (uint32_t)ntiles_of(ch.length, t2);
+        mpk::Tile h1{};
+        h1.signal = L.flags + c;
+        append_tiles(tiles[sp], 2 * round, s0 + ch.offset, (uint64_t)(uintptr_t)stage, ch.length, t1, h1);
+        mpk::Tile h2{};
+        h2.wait = L.flags + c;
+        h2.pass = L.flags + L.flag_cap + c;
+        h2.wait_count = n1;
+        h2.pass_count = n2;
+        h2.flags = mpk::TILE_SRC_MUTABLE;
+        // hop2 of round r is queued after hop1 of round r+1 (overlap, no stall)
+        append_tiles(tiles[rp], 2 * round + 3, (uint64_t)(uintptr_t)stage, d0 + ch.offset, ch.length,
+                     t2, h2);
+      } else {
+        int ev = new_event(sp);
+        e->ce.push_back(CeOp{sp, lane_base[p], stage, (const uint8_t*)src + ch.offset, (size_t)ch.length, -1, ev});
+        e->ce.push_back(CeOp{rp, lane_base[p] + 1, (uint8_t*)dst + ch.offset, stage, (size_t)ch.length, ev, -1});
+      }
+    } else {  // host-staged: D2H into pinned staging, H2D out of it (copy engines)
+      int seq = ch.seq;
+      host_chunk_of_seq.push_back(c);
+      uint8_t* slot;
+      int war = -1;
+      if (host_slots < path_count[p]) {
+        slot = ctx->host_stage + (size_t)(seq % host_slots) * nominal[p];
+        if (seq >= host_slots) war = hop2_done_ev[host_chunk_of_seq[seq - host_slots]];
+      } else {
+        slot = ctx->host_stage + stage_off[p];
+        stage_off[p] += ch.length;
+      }
+      int ev1 = new_event(sp);
+      e->ce.push_back(CeOp{sp, lane_base[p], slot, (const uint8_t*)src + ch.offset, (size_t)ch.length, war, ev1});
+      int ev2 = -1;
+      if (host_slots < path_count[p]) {
+        ev2 = new_event(dp);
+        hop2_done_ev[c] = ev2;
+      }
+      e->ce.push_back(CeOp{dp, lane_base[p] + 1, (uint8_t*)dst + ch.offset, slot, (size_t)ch.length, ev1, ev2});
+    }
+  }
+  // upload one tile table per physical device
+  DeviceGuard g;
+  for (size_t ph = 0; ph < tiles.size(); ++ph) {
+    auto& v = tiles[ph];
+    if (v.empty()) continue;
+    std::stable_sort(v.begin(), v.end(),
+                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::vector<mpk::Tile> flat;
+    flat.reserve(v.size());
+    for (auto& kv : v) flat.push_back(kv.second);
+    Program pr;
+    pr.phys = (int)ph;
+    pr.ntiles = (unsigned)flat.size();
+    Phys& P = ctx->phys[ph];
+    pr.grid = (unsigned)std::min<uint64_t>(flat.size(), (uint64_t)P.sms * std::max(1, o.ctas_per_sm));
+    CK(cudaSetDevice(P.ordinal));
+    CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile)));
+    CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
+    e->progs.push_back(pr);
+  }
+  return e;
+}
+
+// Enqueue the entry's work after `origin`, then make `origin` wait for it.
+void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing) {
+  Phys& S = ctx->phys[e->src_phys];
+  for (auto& p : ctx->phys) p.next_event = 0;
+  CK(cudaSetDevice(S.ordinal));
+  cudaEvent_t fork = take_event(S);
+  CK(cudaEventRecord(fork, origin));
+  std::vector<std::pair<int, cudaStream_t>> used;
+  auto use = [&](int ph, cudaStream_t s) {
+    for (auto& u : used)
+      if (u.second == s) return;
+    CK(cudaSetDevice(ctx->phys[ph].ordinal));
+    CK(cudaStreamWaitEvent(s, fork, 0));
+    used.push_back({ph, s});
+  };
+  // SM transfer kernels, one per physical device
+  for (auto& pr : e->progs) {
+    Phys& P = ctx->phys[pr.phys];
+    use(pr.phys, P.kstream);
+    CK(cudaSetDevice(P.ordinal));
+    bool t = timing && pr.phys == e->src_phys;
+    if (t) CK(cudaEventRecord(P.kt0, P.kstream));
+    mpk::transfer_kernel<kUnroll><<<pr.grid, ctx->opts.threads, 0, P.kstream>>>(pr.d_tiles, pr.ntiles, P.ctl);
+    CK(cudaGetLastError());
+    if (t) CK(cudaEventRecord(P.kt1, P.kstream));
+  }
+  // copy-engine lanes
+  std::vector<cudaEvent_t> evs(e->ev_phys.size());
+  for (size_t i = 0; i < evs.size(); ++i) evs[i] = take_event(ctx->phys[e->ev_phys[i]]);
+  for (const CeOp& op : e->ce) {
+    Phys& P = ctx->phys[op.phys];
+    cudaStream_t s = lane_stream(P, op.lane);
+    use(op.phys, s);
+    CK(cudaSetDevice(P.ordinal));
+    if (op.wait_ev >= 0) CK(cudaStreamWaitEvent(s, evs[op.wait_ev], 0));
+    CK(cudaMemcpyAsync(op.dst, op.src, op.len, cudaMemcpyDefault, s));
+    if (op.record_ev >= 0) CK(cudaEventRecord(evs[op.record_ev], s));
+  }
+  // join
+  for (auto& u : used) {
+    Phys& P = ctx->phys[u.first];
+    CK(cudaSetDevice(P.ordinal));
+    cudaEvent_t j = take_event(P);
+    CK(cudaEventRecord(j, u.second));
+    CK(cudaSetDevice(S.ordinal));
+    CK(cudaStreamWaitEvent(origin, j, 0));
+  }
+  CK(cudaSetDevice(S.ordinal));
+}
+
+void capture(mp_ctx* ctx, Entry* e) {
+  Phys& S = ctx->phys[e->src_phys];
+  CK(cudaSetDevice(S.ordinal));
+  double t0 = now_us();
+  CK(cudaStreamBeginCapture(S.capture, cudaStreamCaptureModeThreadLocal));
+  double t1 = now_us();
+  try {
+    enqueue(ctx, e, S.capture, false);
+  } catch (...) {
+    cudaGraph_t g;
+    cudaStreamEndCapture(S.capture, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  cudaGraph_t graph = nullptr;
+  CK(cudaStreamEndCapture(S.capture, &graph));
+  double t2 = now_us();
+  size_t n = 0;
+  cudaGraphGetNodes(graph, nullptr, &n);
+  e->nodes_physical = (int)n;
+  cudaError_t ie = cudaGraphInstantiate(&e->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ie != cudaSuccess) throw Error{MP_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie)};
+  double t3 = now_us();
+  ctx->stats.creation_us = t1 - t0;
+  ctx->stats.construction_us = t2 - t1;
+  ctx->stats.instantiation_us = t3 - t2;
+}
+
+std::string make_key(const void* src, void* dst, uint64_t size, int sd, int dd, const mp_config& c) {
+  struct {
+    uint64_t s, d, n;
+    int32_t sd, dd, g, h, m, gm, pol;
+  } k{(uint64_t)(uintptr_t)src, (uint64_t)(uintptr_t)dst, size, sd, dd,
+      c.num_gpu_paths, c.host_path_enabled, c.max_chunks, c.graph_mode ? 1 : 0, c.share_policy};
+  return std::string((const char*)&k, sizeof k);
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+#define GUARD_BEGIN try {
+#define GUARD_END                                      \
+  }                                                    \
+  catch (const Error& e) {                             \
+    return fail(e.code, e.msg);                        \
+  }                                                    \
+  catch (const std::exception& e) {                    \
+    return fail(MP_ERR_VALUE, e.what());               \
+  }
+
+extern "C" {
+
+int mp_ctx_create(int32_t n_logical, const int32_t* device_map, mp_ctx** out) {
+  GUARD_BEGIN
+  if (!out || n_logical < 1 || !device_map) return fail(MP_ERR_VALUE, "bad context arguments");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  DeviceGuard g;
+  auto ctx = std::make_unique<mp_ctx>();
+  ctx->opts.direct_engine = MP_ENGINE_SM;
+  ctx->opts.relay_engine = MP_ENGINE_SM;
+  ctx->opts.copy_kind = MP_COPY_VEC;
+  ctx->opts.ctas_per_sm = 2;
+  ctx->opts.threads = 256;
+  ctx->opts.tile_bytes = 0;
+  ctx->opts.host_slots = 0;
+  ctx->opts.pull = 0;
+  ctx->opts.sm_min_bytes = 0;
+  std::map<int, int> phys_of;
+  for (int i = 0; i < n_logical; ++i) {
+    int ord = device_map[i];
+    if (ord < 0 || ord >= ndev)
+      return fail(MP_ERR_VALUE, "device_map[" + std::to_string(i) + "] = " + std::to_string(ord) +
+                                    " is not a CUDA device (have " + std::to_string(ndev) + ")");
+    if (!phys_of.count(ord)) {
+      phys_of[ord] = (int)ctx->phys.size();
+      Phys p;
+      p.ordinal = ord;
+      ctx->phys.push_back(p);
+    }
+    Logi L;
+    L.phys = phys_of[ord];
+    ctx->logi.push_back(L);
+  }
+  const int np = (int)ctx->phys.size();
+  ctx->peer.assign(np * np, 0);
+  for (int a = 0; a < np; ++a) {
+    Phys& P = ctx->phys[a];
+    CK(cudaSetDevice(P.ordinal));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, P.ordinal));
+    P.sms = prop.multiProcessorCount;
+    CK(cudaMalloc(&P.ctl, sizeof(mpk::Ctl)));
+    CK(cudaMemset(P.ctl, 0, sizeof(mpk::Ctl)));
+    CK(cudaStreamCreateWithFlags(&P.kstream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&P.capture, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&P.kt0));
+    CK(cudaEventCreate(&P.kt1));
+    for (int b = 0; b < np; ++b) {
+      if (a == b) {
+        ctx->peer[a * np + b] = 1;
+        continue;
+      }
+      int can = 0;
+      CK(cudaDeviceCanAccessPeer(&can, P.ordinal, ctx->phys[b].ordinal));
+      if (can) {
+        cudaError_t pe = cudaDeviceEnablePeerAccess(ctx->phys[b].ordinal, 0);
+        if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (pe != cudaSuccess) throw Error{MP_ERR_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(pe)};
+      }
+      ctx->peer[a * np + b] = can;
+    }
+  }
+  CK(cudaSetDevice(ctx->phys[0].ordinal));
+  CK(cudaEventCreateWithFlags(&ctx->last_done, cudaEventDisableTiming));
+  CK(cudaDeviceSynchronize());
+  *out = ctx.release();
+  return MP_OK;
+  GUARD_END
+}
+
+void mp_ctx_destroy(mp_ctx* ctx) {
+  if (!ctx) return;
+  clear_cache(ctx);
+  for (auto& L : ctx->logi) {
+    cudaSetDevice(ctx->phys[L.phys].ordinal);
+    if (L.stage) cudaFree(L.stage);
+    if (L.flags) cudaFree(L.flags);
+  }
+  if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+  for (auto& P : ctx->phys) {
+    cudaSetDevice(P.ordinal);
+    for (auto s : P.lanes) cudaStreamDestroy(s);
+    for (auto e : P.events) cudaEventDestroy(e);
+    cudaStreamDestroy(P.kstream);
+    cudaStreamDestroy(P.capture);
+    cudaEventDestroy(P.kt0);
+    cudaEventDestroy(P.kt1);
+    cudaFree(P.ctl);
+  }
+  cudaEventDestroy(ctx->last_done);
+  delete ctx;
+}
+
+int mp_ctx_set_topology(mp_ctx* ctx, const mp_topology* topo) {
+  GUARD_BEGIN
+  if (!ctx || !topo) return fail(MP_ERR_VALUE, "null argument");
+  if (topo->t.n_accel != (int)ctx->logi.size())
+    return fail(MP_ERR_STATE, "topology has " + std::to_string(topo->t.n_accel) +
+                                  " accelerators but the context maps " +
+                                  std::to_string(ctx->logi.size()));
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  clear_cache(ctx);
+  ctx->topo = topo->t;
+  ctx->has_topo = true;
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_ctx_set_engine(mp_ctx* ctx, const mp_engine_opts* o) {
+  GUARD_BEGIN
+  if (!ctx || !o) return fail(MP_ERR_VALUE, "null argument");
+  if (o->threads < 32 || o->threads > 256 || o->threads % 32)
+    return fail(MP_ERR_VALUE, "threads must be a multiple of 32 in [32, 256]");
+  if (o->ctas_per_sm < 1 || o->ctas_per_sm > 8) return fail(MP_ERR_VALUE, "ctas_per_sm must be in [1, 8]");
+  if (o->host_slots == 1) return fail(MP_ERR_VALUE, "host_slots must be 0 (all) or >= 2");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  clear_cache(ctx);
+  ctx->opts = *o;
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_ctx_get_engine(const mp_ctx* ctx, mp_engine_opts* o) {
+  if (!ctx || !o) return fail(MP_ERR_VALUE, "null argument");
+  *o = ctx->opts;
+  return MP_OK;
+}
+
+int mp_ctx_peer_matrix(const mp_ctx* ctx, int32_t* out, int32_t cap) {
+  if (!ctx || !out) return fail(MP_ERR_VALUE, "null argument");
+  if (cap < (int)ctx->peer.size()) return fail(MP_ERR_CAPACITY, "peer matrix capacity too small");
+  for (size_t i = 0; i < ctx->peer.size(); ++i) out[i] = ctx->peer[i];
+  return MP_OK;
+}
+
+int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_dev,
+            int32_t dst_dev, const mp_config* cfg, void* stream) {
+  GUARD_BEGIN
+  if (!ctx || !cfg) return fail(MP_ERR_VALUE, "null argument");
+  if (!ctx->has_topo) return fail(MP_ERR_STATE, "context has no topology (mp_ctx_set_topology)");
+  if (src_dev < 0 || src_dev >= (int)ctx->logi.size() || dst_dev < 0 || dst_dev >= (int)ctx->logi.size()) {
+    if (src_dev == dst_dev)
+      return fail(MP_ERR_PLAN, "source and destination are the same device (" + device_label(src_dev) + ")");
+    return fail(MP_ERR_PLAN, "transfers run between accelerators");
+  }
+  if (size == 0) return fail(MP_ERR_CHUNK, "message size must be >= 1 byte, got 0");
+  if (!src || !dst) return fail(MP_ERR_VALUE, "null buffer");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g;
+  double t_start = now_us();
+  cudaStream_t user = (cudaStream_t)stream;
+  std::string key = make_key(src, dst, size, src_dev, dst_dev, *cfg);
+  Entry* e = nullptr;
+  auto it = ctx->index.find(key);
+  mp_send_stats& st = ctx->stats;
+  if (it != ctx->index.end()) {
+    ctx->lru.splice(ctx->lru.end(), ctx->lru, it->second);
+    e = *it->second;
+    st.hit = 1;
+    st.cache_hits++;
+    st.creation_us = st.construction_us = st.instantiation_us = st.plan_us = 0.0;
+  } else {
+    validate_config(*cfg);
+    e = build_entry(ctx, key, src, dst, size, src_dev, dst_dev, *cfg);
+    double t_plan = now_us();
+    st.plan_us = t_plan - t_start;
+    st.creation_us = st.construction_us = st.instantiation_us = 0.0;
+    if (cfg->graph_mode) {
+      try {
+        capture(ctx, e);
+        e->graph = true;
+      } catch (...) {
+        destroy_entry(ctx, e);
+        throw;
+      }
+    }
+    ctx->lru.push_back(e);
+    ctx->index[key] = std::prev(ctx->lru.end());
+    while ((int)ctx->lru.size() > cfg->cache_capacity) {  // graph.py:184-185
+      Entry* old = ctx->lru.front();
+      ctx->lru.pop_front();
+      ctx->index.erase(old->key);
+      CK(cudaSetDevice(ctx->phys[old->src_phys].ordinal));
+      CK(cudaStreamSynchronize(user));  // old graph may still be replaying
+      destroy_entry(ctx, old);
+      st.cache_evictions++;
+    }
+    st.hit = 0;
+    st.cache_misses++;
+  }
+  Phys& S = ctx->phys[e->src_phys];
+  CK(cudaSetDevice(S.ordinal));
+  // serialise with a send issued on another stream (shared counters/arenas)
+  if (ctx->have_last && ctx->last_stream != stream) CK(cudaStreamWaitEvent(user, ctx->last_done, 0));
+  double t_launch = now_us();
+  bool timing = !cfg->graph_mode;
+  if (cfg->graph_mode && e->graph) {
+    CK(cudaGraphLaunch(e->exec, user));
+    st.ce_copies = (int)e->ce.size();
+  } else {
+    enqueue(ctx, e, user, timing);
+    st.ce_copies = (int)e->ce.size();
+  }
+  CK(cudaEventRecord(ctx->last_done, user));
+  ctx->have_last = true;
+  ctx->last_stream = stream;
+  st.launch_us = now_us() - t_launch;
+  st.graph_mode = cfg->graph_mode ? 1 : 0;
+  st.nodes_logical = e->nodes_logical;
+  st.nodes_physical = e->nodes_physical;
+  st.kernels = (int)e->progs.size();
+  ctx->last_paths = e->paths;
+  ctx->last_chunks = e->chunks;
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_wait(mp_ctx* ctx, void* stream) {
+  GUARD_BEGIN
+  if (!ctx) return fail(MP_ERR_VALUE, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (ctx->have_last) CK(cudaStreamWaitEvent((cudaStream_t)stream, ctx->last_done, 0));
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_send_stats_get(const mp_ctx* ctx, mp_send_stats* out) {
+  if (!ctx || !out) return fail(MP_ERR_VALUE, "null argument");
+  *out = ctx->stats;
+  return MP_OK;
+}
+
+int mp_last_plan(const mp_ctx* ctx, mp_path* paths, int32_t paths_cap, int32_t* n_paths,
+                 mp_chunk* chunks, int32_t chunks_cap, int32_t* n_chunks) {
+  if (!ctx) return fail(MP_ERR_VALUE, "null argument");
+  if (n_paths) *n_paths = (int32_t)ctx->last_paths.size();
+  if (n_chunks) *n_chunks = (int32_t)ctx->last_chunks.size();
+  if (paths_cap < (int)ctx->last_paths.size() || chunks_cap < (int)ctx->last_chunks.size())
+    return fail(MP_ERR_CAPACITY, "plan capacity too small");
+  if (paths && !ctx->last_paths.empty())
+    memcpy(paths, ctx->last_paths.data(), ctx->last_paths.size() * sizeof(mp_path));
+  if (chunks && !ctx->last_chunks.empty())
+    memcpy(chunks, ctx->last_chunks.data(), ctx->last_chunks.size() * sizeof(mp_chunk));
+  return MP_OK;
+}
+
+int mp_cache_clear(mp_ctx* ctx) {
+  GUARD_BEGIN
+  if (!ctx) return fail(MP_ERR_VALUE, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g;
+  clear_cache(ctx);
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_sync(mp_ctx* ctx) {
+  GUARD_BEGIN
+  if (!ctx) return fail(MP_ERR_VALUE, "null argument");
+  DeviceGuard g;
+  for (auto& P : ctx->phys) {
+    CK(cudaSetDevice(P.ordinal));
+    CK(cudaDeviceSynchronize());
+    mpk::Ctl c;
+    CK(cudaMemcpy(&c, P.ctl, sizeof c, cudaMemcpyDeviceToHost));
+    if (c.error) {
+      CK(cudaMemset(P.ctl, 0, sizeof(mpk::Ctl)));
+      return fail(MP_ERR_CUDA, "relay flag wait timed out on device " + std::to_string(P.ordinal));
+    }
+  }
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_kernel_time_ms(const mp_ctx* ctx, double* ms) {
+  GUARD_BEGIN
+  if (!ctx || !ms) return fail(MP_ERR_VALUE, "null argument");
+  DeviceGuard g;
+  const Phys& S = ctx->phys[0];
+  CK(cudaSetDevice(S.ordinal));
+  float f = 0.f;
+  CK(cudaEventSynchronize(S.kt1));
+  CK(cudaEventElapsedTime(&f, S.kt0, S.kt1));
+  *ms = f;
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t bytes, int32_t iters,
+                     double* out_gbps, int32_t cap) {
+  GUARD_BEGIN
+  if (!ctx || !out_gbps || cap < 4) return fail(MP_ERR_VALUE, "need 4 output slots");
+  if (src_dev < 0 || dst_dev < 0 || src_dev >= (int)ctx->logi.size() || dst_dev >= (int)ctx->logi.size())
+    return fail(MP_ERR_VALUE, "device out of range");
+  if (bytes == 0 || iters < 1) return fail(MP_ERR_VALUE, "bytes and iters must be positive");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g;
+  Phys& S = ctx->phys[ctx->logi[src_dev].phys];
+  Phys& D = ctx->phys[ctx->logi[dst_dev].phys];
+  uint8_t *a = nullptr, *b = nullptr, *h = nullptr;
+  CK(cudaSetDevice(S.ordinal));
+  CK(cudaMalloc(&a, bytes));
+  CK(cudaMemset(a, 1, bytes));
+  CK(cudaSetDevice(D.ordinal));
+  CK(cudaMalloc(&b, bytes));
+  CK(cudaHostAlloc((void**)&h, bytes, cudaHostAllocPortable));
+  auto time_it = [&](Phys& P, auto&& fn) {
+    CK(cudaSetDevice(P.ordinal));
+    fn(P.kstream);  // warm-up
+    CK(cudaEventRecord(P.kt0, P.kstream));
+    for (int i = 0; i < iters; ++i) fn(P.kstream);
+    CK(cudaEventRecord(P.kt1, P.kstream));
+    CK(cudaEventSynchronize(P.kt1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, P.kt0, P.kt1));
+    return (double)bytes * iters / (ms * 1e-3) / 1e9;
+  };
+  // direct: the SM transfer kernel over one tile table (same code as mp_send)
+  std::vector<mpk::Tile> flat;
+  uint64_t tile = auto_tile_bytes(ctx, bytes, S.sms);
+  for (uint64_t o = 0; o < bytes; o += tile) {
+    mpk::Tile t{};
+    t.src = (uint64_t)(uintptr_t)(a + o);
+    t.dst = (uint64_t)(uintptr_t)(b + o);
+    t.len = std::min(tile, bytes - o);
+    flat.push_back(t);
+  }
+  mpk::Tile* dt = nullptr;
+  CK(cudaSetDevice(S.ordinal));
+  CK(cudaMalloc(&dt, flat.size() * sizeof(mpk::Tile)));
+  CK(cudaMemcpy(dt, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
+  unsigned grid = (unsigned)std::min<uint64_t>(flat.size(), (uint64_t)S.sms * ctx->opts.ctas_per_sm);
+  out_gbps[0] = time_it(S, [&](cudaStream_t s) {
+    mpk::transfer_kernel<kUnroll><<<grid, ctx->opts.threads, 0, s>>>(dt, (unsigned)flat.size(), S.ctl);
+  });
+  out_gbps[1] = time_it(S, [&](cudaStream_t s) { cudaMemcpyAsync(h, a, bytes, cudaMemcpyDeviceToHost, s); });
+  out_gbps[2] = time_it(D, [&](cudaStream_t s) { cudaMemcpyAsync(b, h, bytes, cudaMemcpyHostToDevice, s); });
+  out_gbps[3] = time_it(S, [&](cudaStream_t s) { cudaMemcpyAsync(b, a, bytes, cudaMemcpyDefault, s); });
+  CK(cudaGetLastError());
+  CK(cudaSetDevice(S.ordinal));
+  CK(cudaDeviceSynchronize());
+  cudaFree(dt);
+  cudaFree(a);
+  cudaSetDevice(D.ordinal);
+  cudaFree(b);
+  cudaFreeHost(h);
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_ipc_export(const void* dev_ptr, int32_t device, uint8_t* handle_out) {
+  GUARD_BEGIN
+  if (!dev_ptr || !handle_out) return fail(MP_ERR_VALUE, "null argument");
+  DeviceGuard g;
+  CK(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  static_assert(sizeof(h) == MP_IPC_HANDLE_BYTES, "ipc handle size");
+  memcpy(handle_out, &h, sizeof h);
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_ipc_import(const uint8_t* handle, int32_t device, void** dev_ptr_out) {
+  GUARD_BEGIN
+  if (!handle || !dev_ptr_out) return fail(MP_ERR_VALUE, "null argument");
+  DeviceGuard g;
+  CK(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  CK(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_ipc_close(void* dev_ptr, int32_t device) {
+  GUARD_BEGIN
+  DeviceGuard g;
+  CK(cudaSetDevice(device));
+  CK(cudaIpcCloseMemHandle(dev_ptr));
+  return MP_OK;
+  GUARD_END
+}
+
+}  // extern "C"

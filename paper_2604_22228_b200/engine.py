@@ -1,0 +1,265 @@
+"""Real multi-path transfers on B200: the `send` / `recv` entry points.
+
+This replaces the reference's simulated execution (`simulate_graph` /
+`simulate_streamed`, /root/reference/pkg/src/mpsim/sim.py:272-292) with the
+CUDA engine behind `mp_send` (csrc/mp_engine.cu):
+
+    plan_paths -> make_chunk_plan           (C++ planner, bit-exact)
+    -> key (src, dst, size, devices, path set) -> LRU of cudaGraphExec_t
+    -> miss: lower to device tiles + copy-engine lanes, capture, instantiate
+    -> hit : one cudaGraphLaunch on the caller's stream
+
+PyTorch only owns the buffers and streams.  Logical accelerators of the
+topology map onto physical CUDA devices through `device_map`; several
+logical devices may share one GPU ("loopback"), which runs every path type —
+relay flags included — on a single B200.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import _lib
+from ._lib import MP_ENGINE_CE, MP_ENGINE_SM, check, lib
+from .paths import PathConfig, _paths_from_abi
+from .pipeline import ChunkAssignment
+from .topology import Topology, load_topology, mesh_text
+
+ENGINES = {"sm": MP_ENGINE_SM, "ce": MP_ENGINE_CE}
+
+
+@dataclass
+class SendStats:
+    """Lifecycle of the last send: the reference's four phases (graph.py:24), measured."""
+
+    hit: bool
+    graph_mode: bool
+    nodes_logical: int
+    nodes_physical: int
+    kernels: int
+    ce_copies: int
+    creation_us: float
+    construction_us: float
+    instantiation_us: float
+    launch_us: float
+    plan_us: float
+    cache_hits: int
+    cache_misses: int
+    cache_evictions: int
+
+
+def _torch():
+    import torch  # noqa: PLC0415 - torch is plumbing, imported on first use
+    return torch
+
+
+class Engine:
+    """A transfer context over `n_logical` accelerators of `topology`."""
+
+    def __init__(self, topology: Topology, device_map: list[int] | None = None):
+        n = len(topology.accelerators)
+        if device_map is None:
+            count = _torch().cuda.device_count()
+            if count < 1:
+                raise _lib.EngineError("no CUDA device is visible: the engine has no CPU path")
+            device_map = [i % count for i in range(n)]
+        if len(device_map) != n:
+            raise ValueError(f"device_map has {len(device_map)} entries for {n} accelerators")
+        self.topology = topology
+        self.device_map = list(device_map)
+        arr = (C.c_int32 * n)(*self.device_map)
+        self._ctx = C.c_void_p()
+        check(lib.mp_ctx_create(n, arr, C.byref(self._ctx)))
+        check(lib.mp_ctx_set_topology(self._ctx, topology._handle))
+
+    @classmethod
+    def loopback(cls, n_logical: int = 2, device: int = 0, link_bw: float = 3.0e12,
+                 host_bw: float = 50e9) -> "Engine":
+        """`n_logical` logical GPUs all mapped onto one physical device."""
+        topo = load_topology(mesh_text("loopback", n_logical, link_bw, 1, 2e-6, host_bw, 10e-6,
+                                       "full"))
+        return cls(topo, [device] * n_logical)
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib.mp_ctx_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- configuration ------------------------------------------------------
+    def set_topology(self, topology: Topology):
+        check(lib.mp_ctx_set_topology(self._ctx, topology._handle))
+        self.topology = topology
+
+    def configure(self, *, direct: str | None = None, relay: str | None = None,
+                  ctas_per_sm: int | None = None, threads: int | None = None,
+                  tile_bytes: int | None = None, host_slots: int | None = None,
+                  pull: bool | None = None, sm_min_bytes: int | None = None) -> None:
+        """Pick the copy mechanism per path type and the SM-kernel shape."""
+        o = _lib.mp_engine_opts()
+        check(lib.mp_ctx_get_engine(self._ctx, C.byref(o)))
+        if direct is not None:
+            o.direct_engine = ENGINES[direct]
+        if relay is not None:
+            o.relay_engine = ENGINES[relay]
+        if ctas_per_sm is not None:
+            o.ctas_per_sm = ctas_per_sm
+        if threads is not None:
+            o.threads = threads
+        if tile_bytes is not None:
+            o.tile_bytes = tile_bytes
+        if host_slots is not None:
+            o.host_slots = host_slots
+        if pull is not None:
+            o.pull = int(pull)
+        if sm_min_bytes is not None:
+            o.sm_min_bytes = sm_min_bytes
+        check(lib.mp_ctx_set_engine(self._ctx, C.byref(o)))
+
+    def options(self) -> dict:
+        o = _lib.mp_engine_opts()
+        check(lib.mp_ctx_get_engine(self._ctx, C.byref(o)))
+        return {f: getattr(o, f) for f, _ in o._fields_}
+
+    # -- the transfer -------------------------------------------------------
+    def send_ptr(self, src_ptr: int, dst_ptr: int, nbytes: int, src_dev: int, dst_dev: int,
+                 config: PathConfig, stream: int = 0) -> None:
+        """Raw-pointer send through the C ABI (`mp_send`)."""
+        cfg = config.abi()
+        check(lib.mp_send(self._ctx, src_ptr, dst_ptr, nbytes, src_dev, dst_dev, C.byref(cfg),
+                          stream or None))
+
+    def send(self, src, dst, nbytes: int | None = None, config: PathConfig | None = None,
+             stream=None, src_dev: int | None = None, dst_dev: int | None = None) -> None:
+        """Move `nbytes` (default: all of `src`) from tensor `src` to tensor `dst`.
+
+        Asynchronous on `stream` (default: the current stream of src's
+        device): ordered after prior work there, and that stream waits for
+        completion.  `src_dev`/`dst_dev` are logical accelerators; by default
+        the first logical device mapped to each tensor's GPU.
+        """
+        torch = _torch()
+        config = config or PathConfig.from_env()
+        if nbytes is None:
+            nbytes = src.numel() * src.element_size()
+        if nbytes > dst.numel() * dst.element_size() or nbytes > src.numel() * src.element_size():
+            raise ValueError("nbytes exceeds a buffer")
+        if src_dev is None:
+            src_dev = self.device_map.index(src.device.index)
+        if dst_dev is None:
+            phys = dst.device.index
+            cands = [i for i, d in enumerate(self.device_map) if d == phys and i != src_dev]
+            if not cands:
+                raise ValueError("cannot infer the logical destination device; pass dst_dev")
+            dst_dev = cands[0]
+        if stream is None:
+            stream = torch.cuda.current_stream(src.device)
+        handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        self.send_ptr(src.data_ptr(), dst.data_ptr(), nbytes, src_dev, dst_dev, config, handle)
+
+    def recv(self, dst, stream=None) -> None:
+        """Single-process mode: `send` already wrote `dst` on the sender's
+        stream; `recv` makes `stream` (default: current stream of dst's
+        device) wait for the last send (`mp_wait`)."""
+        torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream(dst.device)
+        handle = s.cuda_stream if hasattr(s, "cuda_stream") else int(s)
+        check(lib.mp_wait(self._ctx, handle or None))
+
+    def sync(self) -> None:
+        """Wait for every transfer; raises if a relay flag wait timed out."""
+        check(lib.mp_sync(self._ctx))
+
+    # -- introspection -------------------------------------------------------
+    def stats(self) -> SendStats:
+        s = _lib.mp_send_stats()
+        check(lib.mp_send_stats_get(self._ctx, C.byref(s)))
+        return SendStats(bool(s.hit), bool(s.graph_mode), s.nodes_logical, s.nodes_physical,
+                         s.kernels, s.ce_copies, s.creation_us, s.construction_us,
+                         s.instantiation_us, s.launch_us, s.plan_us, s.cache_hits,
+                         s.cache_misses, s.cache_evictions)
+
+    def last_plan(self):
+        """(paths, chunks) the engine executed on the last send — for parity checks."""
+        npaths, nchunks = C.c_int32(), C.c_int32()
+        lib.mp_last_plan(self._ctx, None, 0, C.byref(npaths), None, 0, C.byref(nchunks))
+        paths = (_lib.mp_path * max(1, npaths.value))()
+        chunks = (_lib.mp_chunk * max(1, nchunks.value))()
+        check(lib.mp_last_plan(self._ctx, paths, npaths.value, C.byref(npaths), chunks,
+                               nchunks.value, C.byref(nchunks)))
+        ps = _paths_from_abi(self.topology, paths, npaths.value)
+        cs = tuple(ChunkAssignment(c.path_index, c.offset, c.length, c.seq)
+                   for c in chunks[:nchunks.value])
+        return ps, cs
+
+    def clear_cache(self) -> None:
+        check(lib.mp_cache_clear(self._ctx))
+
+    def kernel_time_ms(self) -> float:
+        ms = C.c_double()
+        check(lib.mp_kernel_time_ms(self._ctx, C.byref(ms)))
+        return ms.value
+
+    def peer_matrix(self) -> list[list[int]]:
+        n = len(set(self.device_map))
+        arr = (C.c_int32 * (n * n))()
+        check(lib.mp_ctx_peer_matrix(self._ctx, arr, n * n))
+        return [list(arr[i * n:(i + 1) * n]) for i in range(n)]
+
+    def measure_paths(self, src_dev: int = 0, dst_dev: int = 1, nbytes: int = 256 << 20,
+                      iters: int = 5) -> dict[str, float]:
+        """GB/s of each path type between two logical devices (1 GB = 1e9 B)."""
+        out = (C.c_double * 4)()
+        check(lib.mp_measure_paths(self._ctx, src_dev, dst_dev, nbytes, iters, out, 4))
+        return {"direct_sm": out[0], "d2h": out[1], "h2d": out[2], "direct_ce": out[3]}
+
+    def probe_topology(self, nbytes: int = 256 << 20, iters: int = 5,
+                       name: str = "probed") -> str:
+        """Write a reference-schema `.topo` from measured bandwidths.
+
+        Bandwidths are written with repr() and sublinks = 1 so the reference
+        loader parses back the identical doubles (SURVEY.md §8c protocol).
+        Only GPU0's links are probed; the node is assumed symmetric (NVSwitch).
+        """
+        n = len(self.topology.accelerators)
+        m = self.measure_paths(0, 1 if n > 1 else 0, nbytes, iters)
+        link = max(m["direct_sm"], m["direct_ce"]) * 1e9
+        host = min(m["d2h"], m["h2d"]) * 1e9
+        return mesh_text(name, n, link, 1, 2e-6, host, 10e-6, "full")
+
+
+_default: Engine | None = None
+
+
+def default_engine() -> Engine:
+    """All visible GPUs with the nominal B200 preset; a 2-GPU loopback on one GPU."""
+    global _default
+    if _default is None:
+        count = _torch().cuda.device_count()
+        if count >= 2:
+            from .topology import preset  # noqa: PLC0415
+            topo = preset("b200") if count == 8 else load_topology(
+                mesh_text("node", count, 900e9, 1, 2e-6, 64e9, 10e-6, "full"))
+            _default = Engine(topo, list(range(count)))
+        else:
+            _default = Engine.loopback(2)
+    return _default
+
+
+def send(src, dst, nbytes: int | None = None, config: PathConfig | None = None, stream=None,
+         src_dev: int | None = None, dst_dev: int | None = None) -> None:
+    """Module-level multi-path send on the default engine (see Engine.send)."""
+    default_engine().send(src, dst, nbytes, config, stream, src_dev, dst_dev)
+
+
+def recv(dst, stream=None) -> None:
+    default_engine().recv(dst, stream)
