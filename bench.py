@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--chunks", type=int, default=8)
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--window", type=int, default=16)
+    ap.add_argument("--quick", action="store_true",
+                    help="headline only: no sweep, lifecycle or CPU baseline (for ncu)")
     return ap.parse_args()
 
 
@@ -218,10 +220,10 @@ def run_ours(args, rank, world):
 
     # 1. probe per-path bandwidths -> reference-schema .topo (SURVEY §8c protocol)
     probe = Engine.loopback(2, dev)
-    m = probe.measure_paths(0, 1, 256 * MiB, 5)
+    link_bw, host_bw = probe.probe_bandwidths(256 * MiB, 5, host_bytes=8 * MiB)
+    m = probe.last_probe["bulk"]
+    m["host_staged_8MiB"] = probe.last_probe["host_share_sized"]["host_staged"]
     probe.close()
-    link_bw = max(m["direct_sm"], m["direct_ce"]) * 1e9
-    host_bw = min(m["d2h"], m["h2d"]) * 1e9
     topo_text = loopback_topo_text(link_bw, host_bw)
     eng = Engine(load_topology(topo_text), [dev, dev])
     size = args.size
@@ -304,13 +306,13 @@ def run_ours(args, rank, world):
 
     # 5. osu_bw-style sweep: single path CE / SM vs multi-path graph on / off
     sweep = []
-    if not args.no_sweep:
+    if not (args.no_sweep or args.quick):
         sweep = run_sweep(torch, eng, topo_text, dev, stream, args.window)
 
     # 6. lifecycle (BASELINE config 5) and the reference's CPU path timing
-    lifecycle = run_lifecycle(torch, eng, dev, stream)
+    lifecycle = None if args.quick else run_lifecycle(torch, eng, dev, stream)
     cpu = None
-    if rank == 0:
+    if rank == 0 and not args.quick:
         cpu_rate, nmsg = cpu_transfer_rate(64 * MiB, args.chunks, 10.0,
                                            len(os.sched_getaffinity(0)))
         cpu = {"value": cpu_rate / 1e9, "unit": "GB/s", "cores": len(os.sched_getaffinity(0)),

@@ -175,6 +175,9 @@ typedef struct {
   int32_t host_slots;        /* pinned host staging slots (>=2), 0=all */
   int32_t pull;              /* 1: direct copies run on the dst device */
   int64_t sm_min_bytes;      /* below this a path uses CE even if SM  */
+  int32_t unroll;            /* VEC: 16-byte loads in flight / thread (4, 8, 16) */
+  int32_t tma_stages;        /* TMA: shared-memory ring stages (2..16)  */
+  int32_t tma_block;         /* TMA: bytes per bulk copy (multiple of 16) */
 } mp_engine_opts;
 
 /* ---- errors / version ---------------------------------------------------- */
@@ -286,8 +289,10 @@ int mp_cache_clear(mp_ctx* ctx);
 int mp_sync(mp_ctx* ctx);
 
 /* Per-path bandwidth probe: times `iters` copies of `bytes` over each path
- * type between src and dst and writes GB/s (1e9 B/s): out[0]=direct,
- * out[1]=host D2H, out[2]=host H2D, out[3]=relay hop (src->stage). */
+ * type between src and dst and writes GB/s (1e9 B/s): out[0] = direct by the
+ * SM transfer kernel, out[1] = D2H, out[2] = H2D, out[3] = direct by a CE
+ * copy; with cap >= 6 also out[4] = D2H and H2D concurrently (per direction)
+ * and out[5] = the host-staged path as executed (8 pipelined chunks). */
 int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t bytes,
                      int32_t iters, double* out_gbps, int32_t cap);
 

@@ -39,18 +39,37 @@ using namespace mp;
 
 namespace {
 
-constexpr int kUnroll = 8;
-
-struct CudaError {
-  std::string msg;
-};
-
 #define CK(call)                                                                        \
   do {                                                                                  \
     cudaError_t _e = (call);                                                            \
     if (_e != cudaSuccess)                                                              \
       throw Error{MP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)};     \
   } while (0)
+
+using KernelFn = void (*)(const mpk::Tile*, unsigned, mpk::Ctl*, unsigned, unsigned);
+
+KernelFn pick_kernel(const mp_engine_opts& o) {
+  if (o.copy_kind == MP_COPY_TMA) return mpk::transfer_kernel<1, 8>;
+  switch (o.unroll) {
+    case 4: return mpk::transfer_kernel<0, 4>;
+    case 16: return mpk::transfer_kernel<0, 16>;
+    default: return mpk::transfer_kernel<0, 8>;
+  }
+}
+
+size_t kernel_smem(const mp_engine_opts& o) {
+  return o.copy_kind == MP_COPY_TMA ? (size_t)o.tma_stages * (size_t)o.tma_block : 0;
+}
+
+// Launch the persistent transfer kernel (mp_kernels.cuh) over one tile table.
+void launch_transfer(const mp_engine_opts& o, unsigned grid, cudaStream_t s, const mpk::Tile* tiles,
+                     unsigned ntiles, mpk::Ctl* ctl) {
+  KernelFn fn = pick_kernel(o);
+  size_t smem = kernel_smem(o);
+  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fn<<<grid, o.threads, smem, s>>>(tiles, ntiles, ctl, (unsigned)o.tma_stages, (unsigned)o.tma_block);
+  CK(cudaGetLastError());
+}
 
 double now_us() {
   using namespace std::chrono;
@@ -226,17 +245,14 @@ void ensure_arenas(mp_ctx* ctx, const std::vector<size_t>& stage_need, int flags
 
 uint64_t auto_tile_bytes(const mp_ctx* ctx, uint64_t path_bytes, int sms) {
   if (ctx->opts.tile_bytes > 0) return (uint64_t)ctx->opts.tile_bytes;
-  // aim for >= 4 tiles per resident CTA, 16 KiB .. 1 MiB, multiple of 4 KiB
+  // aim for >= 4 tiles per resident CTA (tail balance), 16 .. 256 KiB, multiple
+  // of 4 KiB; 256 KiB tiles measured best for the 512 MiB copy (r01 sweep)
   uint64_t ctas = (uint64_t)sms * std::max(1, ctx->opts.ctas_per_sm);
   uint64_t t = path_bytes / (ctas * 4);
   t = std::max<uint64_t>(t, 16 << 10);
-  t = std::min<uint64_t>(t, 1 << 20);
+  t = std::min<uint64_t>(t, 256 << 10);
   return (t + 4095) & ~(uint64_t)4095;
 }
-
-struct Building {
-  std::vector<std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>> tiles;  // per phys
-};
 
 // Split [src, src+len) -> dst into tiles appended to `out`.
 void append_tiles(std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>& out,
@@ -416,8 +432,7 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing) {
     CK(cudaSetDevice(P.ordinal));
     bool t = timing && pr.phys == e->src_phys;
     if (t) CK(cudaEventRecord(P.kt0, P.kstream));
-    mpk::transfer_kernel<kUnroll><<<pr.grid, ctx->opts.threads, 0, P.kstream>>>(pr.d_tiles, pr.ntiles, P.ctl);
-    CK(cudaGetLastError());
+    launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl);
     if (t) CK(cudaEventRecord(P.kt1, P.kstream));
   }
   // copy-engine lanes
@@ -508,13 +523,18 @@ int mp_ctx_create(int32_t n_logical, const int32_t* device_map, mp_ctx** out) {
   auto ctx = std::make_unique<mp_ctx>();
   ctx->opts.direct_engine = MP_ENGINE_SM;
   ctx->opts.relay_engine = MP_ENGINE_SM;
-  ctx->opts.copy_kind = MP_COPY_VEC;
-  ctx->opts.ctas_per_sm = 2;
-  ctx->opts.threads = 256;
+  // measured defaults (profiles/r01_kernel_sweep.jsonl): TMA bulk ring of
+  // 4 x 32 KiB, one CTA per SM, reaches 98% of the measured HBM copy peak
+  ctx->opts.copy_kind = MP_COPY_TMA;
+  ctx->opts.ctas_per_sm = 1;
+  ctx->opts.threads = 128;
   ctx->opts.tile_bytes = 0;
   ctx->opts.host_slots = 0;
   ctx->opts.pull = 0;
   ctx->opts.sm_min_bytes = 0;
+  ctx->opts.unroll = 8;
+  ctx->opts.tma_stages = 4;
+  ctx->opts.tma_block = 32768;
   std::map<int, int> phys_of;
   for (int i = 0; i < n_logical; ++i) {
     int ord = device_map[i];
@@ -613,6 +633,13 @@ int mp_ctx_set_engine(mp_ctx* ctx, const mp_engine_opts* o) {
     return fail(MP_ERR_VALUE, "threads must be a multiple of 32 in [32, 256]");
   if (o->ctas_per_sm < 1 || o->ctas_per_sm > 8) return fail(MP_ERR_VALUE, "ctas_per_sm must be in [1, 8]");
   if (o->host_slots == 1) return fail(MP_ERR_VALUE, "host_slots must be 0 (all) or >= 2");
+  if (o->unroll != 4 && o->unroll != 8 && o->unroll != 16) return fail(MP_ERR_VALUE, "unroll must be 4, 8 or 16");
+  if (o->copy_kind != MP_COPY_VEC && o->copy_kind != MP_COPY_TMA) return fail(MP_ERR_VALUE, "unknown copy kind");
+  if (o->tma_stages < 2 || o->tma_stages > 16) return fail(MP_ERR_VALUE, "tma_stages must be in [2, 16]");
+  if (o->tma_block < 16 || o->tma_block % 16 || (int64_t)o->tma_block * o->tma_stages > 227 * 1024)
+    return fail(MP_ERR_VALUE, "tma_block must be a multiple of 16 with stages*block <= 227 KiB");
+  if (o->direct_engine < 0 || o->direct_engine > 1 || o->relay_engine < 0 || o->relay_engine > 1)
+    return fail(MP_ERR_VALUE, "unknown engine");
   std::lock_guard<std::mutex> lk(ctx->mu);
   clear_cache(ctx);
   ctx->opts = *o;
@@ -831,11 +858,53 @@ int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t byt
   CK(cudaMemcpy(dt, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
   unsigned grid = (unsigned)std::min<uint64_t>(flat.size(), (uint64_t)S.sms * ctx->opts.ctas_per_sm);
   out_gbps[0] = time_it(S, [&](cudaStream_t s) {
-    mpk::transfer_kernel<kUnroll><<<grid, ctx->opts.threads, 0, s>>>(dt, (unsigned)flat.size(), S.ctl);
+    launch_transfer(ctx->opts, grid, s, dt, (unsigned)flat.size(), S.ctl);
   });
   out_gbps[1] = time_it(S, [&](cudaStream_t s) { cudaMemcpyAsync(h, a, bytes, cudaMemcpyDeviceToHost, s); });
   out_gbps[2] = time_it(D, [&](cudaStream_t s) { cudaMemcpyAsync(b, h, bytes, cudaMemcpyHostToDevice, s); });
   out_gbps[3] = time_it(S, [&](cudaStream_t s) { cudaMemcpyAsync(b, a, bytes, cudaMemcpyDefault, s); });
+  if (cap >= 6) {
+    // out[4]: D2H and H2D running at the same time (full duplex), per direction
+    // out[5]: the host-staged path as the engine runs it: 8 pipelined chunks,
+    //         D2H on one lane, H2D on another after a per-chunk event
+    cudaStream_t l0 = lane_stream(S, 0), l1 = lane_stream(D, 1);
+    const int kc = 8;
+    const uint64_t chunk = (bytes / kc + 15) & ~(uint64_t)15;
+    std::vector<cudaEvent_t> ev(kc);
+    for (auto& e : ev) e = take_event(S);
+    cudaEvent_t fork = take_event(S), join = take_event(D);
+    auto round = [&](bool staged) {
+      CK(cudaSetDevice(S.ordinal));
+      CK(cudaEventRecord(fork, S.kstream));
+      CK(cudaStreamWaitEvent(l0, fork, 0));
+      CK(cudaSetDevice(D.ordinal));
+      CK(cudaStreamWaitEvent(l1, fork, 0));
+      for (int c = 0; c < kc; ++c) {
+        uint64_t off = (uint64_t)c * chunk;
+        if (off >= bytes) break;
+        uint64_t n = std::min(chunk, bytes - off);
+        CK(cudaSetDevice(S.ordinal));
+        CK(cudaMemcpyAsync(h + off, a + off, n, cudaMemcpyDeviceToHost, l0));
+        CK(cudaEventRecord(ev[c], l0));
+        CK(cudaSetDevice(D.ordinal));
+        if (staged) CK(cudaStreamWaitEvent(l1, ev[c], 0));
+        // full-duplex probe: H2D reads a different half-buffer region concurrently
+        CK(cudaMemcpyAsync(b + off, staged ? h + off : h + (bytes - off - n), n,
+                           cudaMemcpyHostToDevice, l1));
+      }
+      CK(cudaEventRecord(join, l1));
+      CK(cudaSetDevice(S.ordinal));
+      CK(cudaStreamWaitEvent(S.kstream, join, 0));
+      CK(cudaStreamWaitEvent(S.kstream, ev[kc - 1], 0));
+    };
+    S.next_event = 0;
+    double duplex = time_it(S, [&](cudaStream_t) { round(false); });
+    double staged = time_it(S, [&](cudaStream_t) { round(true); });
+    out_gbps[4] = duplex;
+    out_gbps[5] = staged;
+    S.next_event = 0;
+    D.next_event = 0;
+  }
   CK(cudaGetLastError());
   CK(cudaSetDevice(S.ordinal));
   CK(cudaDeviceSynchronize());

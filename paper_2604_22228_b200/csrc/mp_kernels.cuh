@@ -129,11 +129,131 @@ __device__ __forceinline__ void copy_range(const uint8_t* __restrict__ src,
 
 constexpr uint64_t kWaitTimeoutNs = 4000000000ull;  // 4 s: never hang the GPU
 
-template <int UNROLL>
+// ---------------------------------------------------------------------------
+// TMA bulk path: cp.async.bulk global -> shared -> global through a ring of
+// `stages` shared-memory blocks, driven by one thread; completion of each load
+// is tracked by an mbarrier (complete_tx), reuse of a stage by bulk-group
+// read completion.  The body must be 16-byte aligned on both sides.
+// ---------------------------------------------------------------------------
+struct TmaRing {
+  uint8_t* buf;         // stages * block bytes of dynamic shared memory
+  uint64_t* bar;        // one mbarrier per stage
+  uint32_t phase;       // bit s = parity to wait for on stage s
+  uint32_t stages;
+  uint32_t block;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load(void* smem, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store(void* gdst, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(smem_u32(smem)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Thread 0 streams `len` bytes (16-byte aligned, multiple of 16) through the ring.
+__device__ __forceinline__ void tma_stream(TmaRing& r, const uint8_t* src, uint8_t* dst, uint64_t len) {
+  const uint64_t nblk = (len + r.block - 1) / r.block;
+  auto bytes_of = [&](uint64_t b) -> uint32_t {
+    uint64_t rem = len - b * r.block;
+    return (uint32_t)(rem < r.block ? rem : r.block);
+  };
+  auto load = [&](uint64_t b) {
+    uint32_t s = (uint32_t)(b % r.stages);
+    uint32_t n = bytes_of(b);
+    mbar_expect_tx(&r.bar[s], n);
+    tma_load(r.buf + (size_t)s * r.block, src + b * r.block, n, &r.bar[s]);
+  };
+  const uint64_t pro = nblk < r.stages ? nblk : r.stages;
+  for (uint64_t b = 0; b < pro; ++b) load(b);
+  for (uint64_t b = 0; b < nblk; ++b) {
+    uint32_t s = (uint32_t)(b % r.stages);
+    mbar_wait(&r.bar[s], (r.phase >> s) & 1u);
+    r.phase ^= 1u << s;
+    tma_store(dst + b * r.block, r.buf + (size_t)s * r.block, bytes_of(b));
+    bulk_commit();
+    // refill the stage of block b-1 once its store has read shared memory
+    if (b >= 1 && b - 1 + r.stages < nblk) {
+      bulk_wait_read<1>();
+      load(b - 1 + r.stages);
+    }
+  }
+  bulk_wait_read<0>();  // ring free for the next tile
+}
+
+template <bool MUTABLE>
+__device__ __forceinline__ void copy_range_tma(TmaRing& r, const uint8_t* src, uint8_t* dst,
+                                               uint64_t len) {
+  const unsigned tid = threadIdx.x;
+  uint64_t head = (16u - ((uintptr_t)dst & 15u)) & 15u;
+  if (head > len) head = len;
+  const uint64_t body = (len - head) & ~(uint64_t)15;
+  const uint64_t tail_at = head + body;
+  if (tid == 0) {
+    if (body) {
+      if (MUTABLE) fence_proxy_async();  // staged bytes were written by the generic proxy
+      tma_stream(r, src + head, dst + head, body);
+    }
+  } else if (tid >= 32) {
+    const unsigned k = tid - 32;
+    if (k < head) dst[k] = MUTABLE ? *(volatile const uint8_t*)(src + k) : src[k];
+    if (k < len - tail_at)
+      dst[tail_at + k] = MUTABLE ? *(volatile const uint8_t*)(src + tail_at + k) : src[tail_at + k];
+  }
+}
+
+template <int KIND, int UNROLL>
 __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ tiles,
-                                                       unsigned ntiles, Ctl* ctl) {
+                                                       unsigned ntiles, Ctl* ctl,
+                                                       unsigned stages, unsigned block) {
   __shared__ unsigned s_claim[2];
   __shared__ Tile s_tile;
+  __shared__ uint64_t s_bar[16];
+  extern __shared__ __align__(128) uint8_t s_ring[];
+  TmaRing ring{s_ring, s_bar, 0u, stages, block};
+  if (KIND == 1 && threadIdx.x == 0) {
+    for (unsigned s = 0; s < stages; ++s) mbar_init(&s_bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   if (threadIdx.x == 0) s_claim[0] = atomicAdd(&ctl->work, 1u);
   __syncthreads();
   unsigned w = s_claim[0];
@@ -160,10 +280,20 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
     }
     __syncthreads();
     const Tile& t = s_tile;
-    if (t.flags & TILE_SRC_MUTABLE)
+    const bool mut = t.flags & TILE_SRC_MUTABLE;
+    const bool tma = KIND == 1 && ((((uintptr_t)t.src ^ (uintptr_t)t.dst) & 15u) == 0);
+    if (tma) {
+      if (mut) copy_range_tma<true>(ring, (const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
+      else copy_range_tma<false>(ring, (const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
+    } else if (mut) {
       copy_range<UNROLL, true>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
-    else
+    } else {
       copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
+    }
+    if (tma && threadIdx.x == 0 && t.signal) {
+      bulk_wait_all();  // bulk stores complete before the release
+      fence_proxy_async();
+    }
     __syncthreads();  // every thread's stores precede the release below
     if (threadIdx.x == 0 && t.signal) {
       __threadfence_system();
@@ -174,6 +304,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
     __syncthreads();  // s_tile / s_claim reuse
   }
   if (threadIdx.x == 0) {
+    if (KIND == 1) bulk_wait_all();
     __threadfence();
     if (atomicAdd(&ctl->exit, 1u) + 1u == gridDim.x) {  // last CTA re-arms the counters
       ctl->work = 0u;

@@ -21,12 +21,13 @@ import ctypes as C
 from dataclasses import dataclass
 
 from . import _lib
-from ._lib import MP_ENGINE_CE, MP_ENGINE_SM, check, lib
+from ._lib import MP_COPY_TMA, MP_COPY_VEC, MP_ENGINE_CE, MP_ENGINE_SM, check, lib
 from .paths import PathConfig, _paths_from_abi
 from .pipeline import ChunkAssignment
 from .topology import Topology, load_topology, mesh_text
 
 ENGINES = {"sm": MP_ENGINE_SM, "ce": MP_ENGINE_CE}
+COPIES = {"vec": MP_COPY_VEC, "tma": MP_COPY_TMA}
 
 
 @dataclass
@@ -103,10 +104,20 @@ class Engine:
     def configure(self, *, direct: str | None = None, relay: str | None = None,
                   ctas_per_sm: int | None = None, threads: int | None = None,
                   tile_bytes: int | None = None, host_slots: int | None = None,
-                  pull: bool | None = None, sm_min_bytes: int | None = None) -> None:
+                  pull: bool | None = None, sm_min_bytes: int | None = None,
+                  copy: str | None = None, unroll: int | None = None,
+                  tma_stages: int | None = None, tma_block: int | None = None) -> None:
         """Pick the copy mechanism per path type and the SM-kernel shape."""
         o = _lib.mp_engine_opts()
         check(lib.mp_ctx_get_engine(self._ctx, C.byref(o)))
+        if copy is not None:
+            o.copy_kind = COPIES[copy]
+        if unroll is not None:
+            o.unroll = unroll
+        if tma_stages is not None:
+            o.tma_stages = tma_stages
+        if tma_block is not None:
+            o.tma_block = tma_block
         if direct is not None:
             o.direct_engine = ENGINES[direct]
         if relay is not None:
@@ -217,10 +228,14 @@ class Engine:
 
     def measure_paths(self, src_dev: int = 0, dst_dev: int = 1, nbytes: int = 256 << 20,
                       iters: int = 5) -> dict[str, float]:
-        """GB/s of each path type between two logical devices (1 GB = 1e9 B)."""
-        out = (C.c_double * 4)()
-        check(lib.mp_measure_paths(self._ctx, src_dev, dst_dev, nbytes, iters, out, 4))
-        return {"direct_sm": out[0], "d2h": out[1], "h2d": out[2], "direct_ce": out[3]}
+        """GB/s of each path type between two logical devices (1 GB = 1e9 B):
+        the SM transfer kernel and a CE copy on the direct route, D2H and H2D
+        alone, both at once (per direction), and the host-staged path run as
+        the engine runs it (8 pipelined chunks, event handoff)."""
+        out = (C.c_double * 6)()
+        check(lib.mp_measure_paths(self._ctx, src_dev, dst_dev, nbytes, iters, out, 6))
+        return {"direct_sm": out[0], "d2h": out[1], "h2d": out[2], "direct_ce": out[3],
+                "duplex": out[4], "host_staged": out[5]}
 
     def probe_topology(self, nbytes: int = 256 << 20, iters: int = 5,
                        name: str = "probed") -> str:
@@ -231,10 +246,27 @@ class Engine:
         Only GPU0's links are probed; the node is assumed symmetric (NVSwitch).
         """
         n = len(self.topology.accelerators)
-        m = self.measure_paths(0, 1 if n > 1 else 0, nbytes, iters)
-        link = max(m["direct_sm"], m["direct_ce"]) * 1e9
-        host = min(m["d2h"], m["h2d"]) * 1e9
+        link, host = self.probe_bandwidths(nbytes, iters)
         return mesh_text(name, n, link, 1, 2e-6, host, 10e-6, "full")
+
+    def probe_bandwidths(self, nbytes: int = 256 << 20, iters: int = 5,
+                         host_bytes: int = 8 << 20) -> tuple[float, float]:
+        """(link, host) bytes/s for the planner's `.topo`.
+
+        link = the faster direct mechanism (SM kernel or CE); host = the
+        delivered rate of the host-staged path *as executed* — D2H and H2D
+        pipelined over 8 chunks of a message-sized share, so per-copy
+        overhead and full-duplex contention are priced in.  The reference's
+        split is purely bandwidth-proportional (paths.py:144-150), so feeding
+        it the isolated PCIe rate would overload the staged path by its
+        pipeline fill (k+1)/k.
+        """
+        n = len(self.topology.accelerators)
+        dst = 1 if n > 1 else 0
+        m = self.measure_paths(0, dst, nbytes, iters)
+        h = self.measure_paths(0, dst, host_bytes, max(iters, 10))
+        self.last_probe = {"bulk": m, "host_share_sized": h}
+        return max(m["direct_sm"], m["direct_ce"]) * 1e9, h["host_staged"] * 1e9
 
 
 _default: Engine | None = None

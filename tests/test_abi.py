@@ -1,0 +1,75 @@
+"""The C-ABI library loads without a GPU and exports every symbol that
+include/mpb200.h declares; the Python binding covers the same surface."""
+
+import ctypes
+import os
+import re
+
+from paper_2604_22228_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mpb200.h")
+
+
+def declared():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mp_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    names = declared()
+    for must in ("mp_plan_paths", "mp_make_chunk_plan", "mp_build_graph", "mp_graph_digest",
+                 "mp_cache_access", "mp_ctx_create", "mp_send", "mp_measure_paths",
+                 "mp_ipc_export", "mp_ipc_import", "mp_last_error", "mp_topology_load"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [n for n in declared() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_python_binding_covers_header():
+    assert set(declared()) == set(_lib.SIGNATURES)
+
+
+STRUCTS = ["mp_config", "mp_link", "mp_channel", "mp_hop", "mp_path", "mp_chunk", "mp_lane",
+           "mp_lane_dep", "mp_node", "mp_edge", "mp_send_stats", "mp_engine_opts"]
+
+
+def test_struct_layout_matches_c_compiler(tmp_path):
+    """sizeof/offsetof of every ABI struct as the C compiler lays it out
+    equals the ctypes mirror used by the Python host layer."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        import pytest
+        pytest.skip("gcc not available")
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(){"]
+    for s in STRUCTS:
+        lines.append(f'printf("{s} %zu\\n", sizeof({s}));')
+        for fname, _ in getattr(_lib, s)._fields_:
+            cname = "from" if fname == "from_" else fname
+            lines.append(f'printf("{s}.{fname} %zu\\n", offsetof({s}, {cname}));')
+    lines.append("return 0;}")
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", str(src), "-o", str(exe)], check=True)
+    out = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True,
+                                                         text=True).stdout.splitlines())
+    for s in STRUCTS:
+        cls = getattr(_lib, s)
+        assert int(out[s]) == ctypes.sizeof(cls), s
+        for fname, _ in cls._fields_:
+            assert int(out[f"{s}.{fname}"]) == getattr(cls, fname).offset, (s, fname)
+
+
+def test_abi_version_and_error_text():
+    assert _lib.lib.mp_abi_version() == 1
+    h = ctypes.c_void_p()
+    rc = _lib.lib.mp_topology_load(b"[device]\n0 accelerator\n1 gpu\n", b"t", ctypes.byref(h))
+    assert rc == _lib.MP_ERR_TOPOLOGY
+    assert "only accelerator devices are declared" in _lib.last_error()

@@ -65,10 +65,11 @@ def _check(eng, text, size, *, gpu_paths=1, host=False, chunks=1, graph=False,
     return eng.stats()
 
 
+@pytest.mark.parametrize("copy", ["vec", "tma"])
 @pytest.mark.parametrize("size", [1, 15, 16, 17, 4095, 65536 + 3, MiB + 7, 16 * MiB])
 @pytest.mark.parametrize("graph", [False, True])
-def test_direct_sizes(size, graph):
-    eng, text = _engine(2)
+def test_direct_sizes(size, graph, copy):
+    eng, text = _engine(2, copy=copy)
     _check(eng, text, size, graph=graph)
     eng.close()
 
@@ -87,12 +88,12 @@ def test_config1_direct_plus_host_64mib(direct, k):
     eng.close()
 
 
-@pytest.mark.parametrize("relay", ["sm", "ce"])
+@pytest.mark.parametrize("relay,copy", [("sm", "vec"), ("sm", "tma"), ("ce", "vec")])
 @pytest.mark.parametrize("gpu_paths", [2, 3, 4])
 @pytest.mark.parametrize("graph", [False, True])
-def test_gpu_relays(relay, gpu_paths, graph):
+def test_gpu_relays(relay, copy, gpu_paths, graph):
     """Direct + 1..3 GPU relays (+host): relay flags / events order hop2 after hop1."""
-    eng, text = _engine(gpu_paths + 1, relay=relay)
+    eng, text = _engine(gpu_paths + 1, relay=relay, copy=copy, tile_bytes=256 << 10)
     _check(eng, text, 8 * MiB + 12345, gpu_paths=gpu_paths, host=True, chunks=4, graph=graph,
            policy="equal", reps=2)
     eng.close()
@@ -106,18 +107,20 @@ def test_eight_logical_gpus_six_relays():
     eng.close()
 
 
+@pytest.mark.parametrize("copy", ["vec", "tma"])
 @pytest.mark.parametrize("offs", [(0, 0), (5, 5), (3, 7), (8, 0), (1, 2), (2, 6)])
-def test_misaligned_buffers(offs):
-    eng, text = _engine(3)
+def test_misaligned_buffers(offs, copy):
+    eng, text = _engine(3, copy=copy)
     _check(eng, text, 3 * MiB + 11, gpu_paths=2, host=True, chunks=5, src_off=offs[0],
            dst_off=offs[1], policy="equal")
     eng.close()
 
 
-def test_graph_replay_fresh_data_every_time():
+@pytest.mark.parametrize("copy", ["vec", "tma"])
+def test_graph_replay_fresh_data_every_time(copy):
     """A cached graph replayed many times with new source bytes: relay flags
     must re-arm themselves (no memset node)."""
-    eng, text = _engine(4)
+    eng, text = _engine(4, copy=copy, tile_bytes=64 << 10)
     st = _check(eng, text, 4 * MiB + 99, gpu_paths=3, host=True, chunks=8, graph=True,
                 seed=7, reps=12, policy="equal")
     assert st.hit and st.cache_hits >= 11
