@@ -197,36 +197,67 @@ def workload_config(args):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def time_sends(torch, eng, cfg, src, dst, size, steps, warmup, stream, window=1):
+def time_sends(torch, eng, cfg, src, dst, size, steps, warmup, stream):
     for _ in range(warmup):
         eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(steps * window):
+    for _ in range(steps):
         eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
     e1.record(stream)
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / 1e3 / (steps * window)
+    return e0.elapsed_time(e1) / 1e3 / steps
+
+
+def ncu_traffic():
+    """dram bytes per launch of transfer_kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "transfer_kernel_ncu.json")) as fh:
+            d = json.load(fh)
+        return d["dram_bytes_read"] + d["dram_bytes_write"], d
+    except (OSError, KeyError, ValueError):
+        return None, None
+
+
+def reference_cpu_path(topo_text, size, chunks):
+    """The unmodified reference's per-message CPU path, timed on one host core."""
+    ref = os.path.join(ROOT, "baseline", "_ref", "mpsim")
+    if not os.path.isdir(ref):
+        return {"unavailable": "baseline/_ref not installed"}
+    import tempfile
+    with tempfile.NamedTemporaryFile("w", suffix=".topo", delete=False) as fh:
+        fh.write(topo_text)
+    try:
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ref_cpu_path.py"),
+                              fh.name, str(size), str(chunks)], capture_output=True, text=True,
+                             timeout=300)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as exc:  # noqa: BLE001
+        return {"unavailable": str(exc)[:200]}
+    finally:
+        os.unlink(fh.name)
 
 
 def run_ours(args, rank, world):
     import torch
 
-    from paper_2604_22228_b200 import Engine, PathConfig, load_topology
+    from paper_2604_22228_b200 import Engine, PathConfig
+    from paper_2604_22228_b200.tuner import calibrate_host_bandwidth
     dev = rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
     hbm_peak, peak_kind = peaks()
-
-    # 1. probe per-path bandwidths -> reference-schema .topo (SURVEY §8c protocol)
-    probe = Engine.loopback(2, dev)
-    link_bw, host_bw = probe.probe_bandwidths(256 * MiB, 5, host_bytes=8 * MiB)
-    m = probe.last_probe["bulk"]
-    m["host_staged_8MiB"] = probe.last_probe["host_share_sized"]["host_staged"]
-    probe.close()
-    topo_text = loopback_topo_text(link_bw, host_bw)
-    eng = Engine(load_topology(topo_text), [dev, dev])
     size = args.size
+
+    # 1. probe per-path bandwidths, then calibrate the host link's effective
+    #    rate for the planner's .topo (SURVEY §8c protocol: repr() bandwidths)
+    eng = Engine.loopback(2, dev)
+    link_bw, _ = eng.probe_bandwidths(256 * MiB, 5, host_bytes=8 * MiB)
+    m = dict(eng.last_probe["bulk"])
+    m["host_staged_8MiB"] = eng.last_probe["host_share_sized"]["host_staged"]
+    host_bw, topo, trials = calibrate_host_bandwidth(eng, link_bw, size, args.chunks,
+                                                     name="b200_loopback")
+    topo_text = loopback_topo_text(link_bw, host_bw)
     cfg = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=args.chunks,
                      graph_mode=True)
     src = torch.empty(size, dtype=torch.uint8, device=f"cuda:{dev}")
@@ -249,7 +280,7 @@ def run_ours(args, rank, world):
     direct_bytes = sum(c[2] for c in ochunks if c[0] == 0)
     host_bytes = size - direct_bytes
 
-    # 2. headline: K steps of graph replay, device time, clocks sampled
+    # 2. headline: K steps of cached-graph replay, device time, clocks sampled
     for _ in range(args.warmup):
         eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
     torch.cuda.synchronize()
@@ -269,58 +300,64 @@ def run_ours(args, rank, world):
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t = float(tt)
     value = world * args.steps * size / t / 1e9
+    single_t = time_sends(torch, eng, PathConfig(max_chunks=1, graph_mode=True), src, dst,
+                          size, args.steps, 3, stream)
 
     # 3. dominant kernel: transfer_kernel duration (events on its stream, streamed mode)
     cfg_s = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=args.chunks,
                        graph_mode=False)
     ktimes = []
-    for _ in range(max(3, args.steps // 2)):
+    for _ in range(max(4, args.steps // 2)):
         eng.send(src, dst, size, cfg_s, stream=stream, src_dev=0, dst_dev=1)
         ktimes.append(eng.kernel_time_ms())
     kms = statistics.mean(ktimes[1:])
     k_alg_bytes = 2 * direct_bytes  # HBM read + write of the direct share
     achieved = k_alg_bytes / (kms / 1e3) / 1e9
-    path_roofline = hbm_peak / 2 + min(m["d2h"], m["h2d"])
+    pcie = min(m["d2h"], m["h2d"])
+    path_roofline = hbm_peak / 2 + pcie
+    traffic, ncu = ncu_traffic()
 
-    # 4. e2e through the public API with host buffers
+    # 4. e2e through the public API: H2D of the message from pinned host memory,
+    #    the multi-path send, and a D2H of the step's result (a device checksum)
     hsrc = torch.empty(size, dtype=torch.uint8, pin_memory=True)
-    hdst = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+    hsum = torch.empty(1, dtype=torch.int64, pin_memory=True)
     hsrc.copy_(src.cpu())
+    want = int(src.sum(dtype=torch.int64))
     e2e_steps = max(3, args.steps // 4)
-    for _ in range(2):
+    cur = torch.cuda.current_stream()
+
+    def e2e_step():
         src.copy_(hsrc, non_blocking=True)
         eng.send(src, dst, size, cfg, src_dev=0, dst_dev=1)
-        hdst.copy_(dst, non_blocking=True)
+        hsum.copy_(dst.sum(dtype=torch.int64).view(1), non_blocking=True)
+    for _ in range(2):
+        e2e_step()
     torch.cuda.synchronize()
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    cur = torch.cuda.current_stream()
     c0.record(cur)
     for _ in range(e2e_steps):
-        src.copy_(hsrc, non_blocking=True)
-        eng.send(src, dst, size, cfg, src_dev=0, dst_dev=1)
-        hdst.copy_(dst, non_blocking=True)
+        e2e_step()
     c1.record(cur)
     torch.cuda.synchronize()
     e2e = e2e_steps * size / (c0.elapsed_time(c1) / 1e3) / 1e9
-    assert torch.equal(hdst, hsrc)
+    assert int(hsum) == want
 
-    # 5. osu_bw-style sweep: single path CE / SM vs multi-path graph on / off
-    sweep = []
+    # 5. osu_bw-style sweep and a measured tuning table
+    sweep, tuning = [], None
     if not (args.no_sweep or args.quick):
-        sweep = run_sweep(torch, eng, topo_text, dev, stream, args.window)
+        sweep, tuning = run_sweep(torch, eng, topo_text, dev, stream)
 
-    # 6. lifecycle (BASELINE config 5) and the reference's CPU path timing
+    # 6. lifecycle (BASELINE config 5) and the reference's CPU path
     lifecycle = None if args.quick else run_lifecycle(torch, eng, dev, stream)
-    cpu = None
+    cpu, ref_cpu = None, None
     if rank == 0 and not args.quick:
-        cpu_rate, nmsg = cpu_transfer_rate(64 * MiB, args.chunks, 10.0,
-                                           len(os.sched_getaffinity(0)))
+        cpu_rate, nmsg = cpu_transfer_rate(size, args.chunks, 10.0, len(os.sched_getaffinity(0)))
         cpu = {"value": cpu_rate / 1e9, "unit": "GB/s", "cores": len(os.sched_getaffinity(0)),
-               "kind": "port", "sample": f"{nmsg} x 64 MiB messages, direct+host plan, "
+               "kind": "port", "sample": f"{nmsg} x {size} B messages, direct+host plan, "
                                          "oracle/transfer.py numpy copies, ~10 s", **cpu_info()}
+        ref_cpu = reference_cpu_path(topo_text, size, args.chunks)
     if rank != 0:
         return
-    launches = args.steps * st.kernels
     out = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
@@ -328,22 +365,28 @@ def run_ours(args, rank, world):
         "data": "synthetic (seeded random bytes, seed 20261017)",
         "config": workload_config(args),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
-                     "kernel": "mpk::transfer_kernel<8>", "kernel_ms": kms,
-                     "alg_bytes_per_launch": k_alg_bytes, "peak_kind": peak_kind},
+                     "frac": achieved / hbm_peak, "traffic": traffic,
+                     "kernel": "mpk::transfer_kernel<1,8> (TMA bulk ring)", "kernel_ms": kms,
+                     "alg_bytes_per_launch": k_alg_bytes, "peak_kind": peak_kind,
+                     "traffic_source": ncu and ncu.get("source")},
         "path_roofline": {"R_gbs": path_roofline, "frac": value / path_roofline,
-                          "hbm_copy_gbs": hbm_peak / 2, "pcie_gbs": min(m["d2h"], m["h2d"]),
-                          "probe": m, "direct_bytes": direct_bytes, "host_bytes": host_bytes},
+                          "hbm_copy_gbs": hbm_peak / 2, "pcie_gbs": pcie, "probe": m,
+                          "direct_bytes": direct_bytes, "host_bytes": host_bytes,
+                          "host_bw_calibrated": host_bw, "link_bw": link_bw,
+                          "calibration": trials,
+                          "single_path_sm_gbs": size / single_t / 1e9},
         "cpu_baseline": cpu,
+        "reference_cpu_path_us": ref_cpu,
         "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": size,
-                "d2h_bytes_per_step": size},
-        "gpu_launches": launches,
+                "d2h_bytes_per_step": 8, "result": "int64 checksum of the delivered buffer"},
+        "gpu_launches": args.steps * st.kernels,
         "clocks": clk.summary(),
         "graph": {"nodes_logical": st.nodes_logical, "nodes_physical": st.nodes_physical,
                   "kernels_per_send": st.kernels, "ce_copies_per_send": st.ce_copies,
                   "launch_us": st.launch_us},
         "lifecycle": lifecycle,
         "sweep": sweep,
+        "tuning_csv": tuning,
     }
     print(json.dumps(out), flush=True)
 
@@ -351,33 +394,42 @@ def run_ours(args, rank, world):
 SWEEP_SIZES = [1 << k for k in range(10, 30)]
 
 
-def run_sweep(torch, eng, topo_text, dev, stream, window):
+def run_sweep(torch, eng, topo_text, dev, stream):
+    """osu_bw-style: per size, single path (CE copy = cudaMemcpy, SM kernel),
+    direct+host multi-path with the graph cache on / off, and the measured
+    tuner's best configuration."""
     from paper_2604_22228_b200 import Engine, PathConfig, load_topology
-    rows = []
+    from paper_2604_22228_b200.tuner import GridPoint, tune
     ce = Engine(load_topology(topo_text), [dev, dev])
     ce.configure(direct="ce")
-    single_ce = PathConfig(max_chunks=1, graph_mode=False)
-    single_sm = PathConfig(max_chunks=1, graph_mode=True)
-    multi_g = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=8, graph_mode=True)
-    multi_s = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=8, graph_mode=False)
+    grid = [GridPoint(1, h, c) for h in (False, True) for c in (1, 2, 4, 8, 16, 32)]
+    table = tune(eng, SWEEP_SIZES, grid, modes=("graph",), reps=5)
+    rows = []
     big = torch.empty(SWEEP_SIZES[-1], dtype=torch.uint8, device=f"cuda:{dev}")
     out = torch.empty_like(big)
+    arms = (("ce_single", ce, PathConfig(max_chunks=1, graph_mode=False)),
+            ("sm_single", eng, PathConfig(max_chunks=1, graph_mode=True)),
+            ("multi_graph", eng, PathConfig(1, True, 8, True)),
+            ("multi_stream", eng, PathConfig(1, True, 8, False)))
     for size in SWEEP_SIZES:
         src, dst = big[:size], out[:size]
         steps = 20 if size > MiB else 100
-        warm = 2 if size > MiB else 10
+        warm = 3 if size > MiB else 10
         row = {"bytes": size}
-        for name, e, cfg in (("ce_single", ce, single_ce), ("sm_single", eng, single_sm),
-                             ("multi_graph", eng, multi_g), ("multi_stream", eng, multi_s)):
-            s = time_sends(torch, e, cfg, src, dst, size, steps, warm, stream, window=1)
-            row[name] = size / s / 1e9
+        for name, e, cfg in arms:
+            row[name] = size / time_sends(torch, e, cfg, src, dst, size, steps, warm, stream) / 1e9
+        best = table.lookup(size, "graph").best
+        row["tuned"] = size / time_sends(torch, eng, table.config_for(size), src, dst, size,
+                                         steps, warm, stream) / 1e9
+        row["tuned_point"] = [best.gpu_paths, best.host, best.max_chunks]
         rows.append(row)
     ce.close()
-    return rows
+    return rows, table.to_csv()
 
 
 def run_lifecycle(torch, eng, dev, stream):
-    """Capture+instantiate / cached replay / per-call stream launch, host us per message."""
+    """Capture+instantiate every call / cached replay / per-call stream launch:
+    host us per message, GPU latency, and the four lifecycle phases."""
     from paper_2604_22228_b200 import PathConfig
     res = []
     big = torch.empty(4 * MiB, dtype=torch.uint8, device=f"cuda:{dev}")
@@ -387,7 +439,6 @@ def run_lifecycle(torch, eng, dev, stream):
         g = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=1, graph_mode=True)
         s = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=1, graph_mode=False)
         row = {"bytes": size}
-        # (a) capture + instantiate every call
         cap = []
         for _ in range(20):
             eng.clear_cache()
@@ -396,12 +447,9 @@ def run_lifecycle(torch, eng, dev, stream):
             cap.append((st.creation_us, st.construction_us, st.instantiation_us, st.launch_us,
                         st.plan_us))
         row["capture_every_call_us"] = {
-            "creation": statistics.median(c[0] for c in cap),
-            "construction": statistics.median(c[1] for c in cap),
-            "instantiation": statistics.median(c[2] for c in cap),
-            "launch": statistics.median(c[3] for c in cap),
-            "plan": statistics.median(c[4] for c in cap)}
-        # (b) cached replay, (c) per-call stream launch: host us per message + device latency
+            k: statistics.median(c[i] for c in cap)
+            for i, k in enumerate(("creation", "construction", "instantiation", "launch",
+                                   "plan"))}
         for name, cfg in (("replay", g), ("stream", s)):
             for _ in range(10):
                 eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
@@ -421,8 +469,9 @@ def run_lifecycle(torch, eng, dev, stream):
                 e1.synchronize()
                 lat.append(e0.elapsed_time(e1) * 1e3)
             row[name] = {"host_us_per_msg": host_us, "gpu_latency_us": statistics.median(lat),
-                         "launch_us": eng.stats().launch_us}
+                         "launch_us_c_abi": eng.stats().launch_us}
         row["nodes_logical"] = eng.stats().nodes_logical
+        row["nodes_physical"] = eng.stats().nodes_physical
         res.append(row)
     return res
 

@@ -178,6 +178,8 @@ typedef struct {
   int32_t unroll;            /* VEC: 16-byte loads in flight / thread (4, 8, 16) */
   int32_t tma_stages;        /* TMA: shared-memory ring stages (2..16)  */
   int32_t tma_block;         /* TMA: bytes per bulk copy (multiple of 16) */
+  int32_t host_engine;       /* MP_ENGINE_*: host-staged path by the SM
+                                kernels (mapped pinned memory) or by CEs */
 } mp_engine_opts;
 
 /* ---- errors / version ---------------------------------------------------- */

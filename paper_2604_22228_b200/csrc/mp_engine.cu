@@ -205,18 +205,18 @@ void clear_cache(mp_ctx* ctx) {
 }
 
 // Grow staging arenas; cached programs point into them, so growth drops the cache.
-void ensure_arenas(mp_ctx* ctx, const std::vector<size_t>& stage_need, int flags_need,
-                   size_t host_need) {
+void ensure_arenas(mp_ctx* ctx, const std::vector<size_t>& stage_need,
+                   const std::vector<char>& flag_devs, int flags_need, size_t host_need) {
   bool grow = host_need > ctx->host_cap;
   for (size_t i = 0; i < ctx->logi.size(); ++i)
-    if (stage_need[i] > ctx->logi[i].stage_cap || (stage_need[i] && flags_need > ctx->logi[i].flag_cap))
+    if (stage_need[i] > ctx->logi[i].stage_cap || (flag_devs[i] && flags_need > ctx->logi[i].flag_cap))
       grow = true;
   if (!grow) return;
   clear_cache(ctx);
   DeviceGuard g;
   for (size_t i = 0; i < ctx->logi.size(); ++i) {
     Logi& L = ctx->logi[i];
-    if (stage_need[i] == 0) continue;
+    if (stage_need[i] == 0 && !flag_devs[i]) continue;
     CK(cudaSetDevice(ctx->phys[L.phys].ordinal));
     if (stage_need[i] > L.stage_cap) {
       if (L.stage) CK(cudaFree(L.stage));
@@ -225,7 +225,7 @@ void ensure_arenas(mp_ctx* ctx, const std::vector<size_t>& stage_need, int flags
       CK(cudaMalloc(&L.stage, cap));
       L.stage_cap = cap;
     }
-    if (flags_need > L.flag_cap) {
+    if (flag_devs[i] && flags_need > L.flag_cap) {
       if (L.flags) CK(cudaFree(L.flags));
       int cap = std::max(flags_need, 2 * L.flag_cap);
       CK(cudaMalloc(&L.flags, (size_t)cap * 2 * sizeof(uint32_t)));
@@ -242,6 +242,9 @@ void ensure_arenas(mp_ctx* ctx, const std::vector<size_t>& stage_need, int flags
     ctx->host_cap = cap;
   }
 }
+
+// Host-path tiles stay small so many CTAs keep PCIe requests in flight.
+constexpr uint64_t kHostTileBytes = 64 << 10;
 
 uint64_t auto_tile_bytes(const mp_ctx* ctx, uint64_t path_bytes, int sms) {
   if (ctx->opts.tile_bytes > 0) return (uint64_t)ctx->opts.tile_bytes;
@@ -291,18 +294,29 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
     nominal[c.path_index] = std::max<uint64_t>(nominal[c.path_index], c.length);
     path_count[c.path_index] += 1;
   }
+  // engines per path type for this message size (measured thresholds)
+  const bool sm_ok = size >= (uint64_t)o.sm_min_bytes;
+  const bool direct_sm = o.direct_engine == MP_ENGINE_SM && sm_ok;
+  const bool relay_sm = o.relay_engine == MP_ENGINE_SM && sm_ok;
+  const bool host_sm = o.host_engine == MP_ENGINE_SM && sm_ok;
   // staging requirements
   std::vector<size_t> stage_need(ctx->logi.size(), 0);
+  std::vector<char> flag_devs(ctx->logi.size(), 0);
   size_t host_need = 0;
   int host_slots = 0;
   for (int p = 0; p < np; ++p) {
-    if (e->paths[p].kind == MP_PATH_GPU) stage_need[e->paths[p].stage] = path_bytes[p];
+    if (e->paths[p].kind == MP_PATH_GPU) {
+      stage_need[e->paths[p].stage] = path_bytes[p];
+      if (relay_sm) flag_devs[e->paths[p].stage] = 1;
+    }
     if (e->paths[p].kind == MP_PATH_HOST) {
-      host_slots = o.host_slots > 0 ? std::min(o.host_slots, path_count[p]) : path_count[p];
+      // the SM host path keeps every chunk resident (its share is a few MB)
+      host_slots = (o.host_slots > 0 && !host_sm) ? std::min(o.host_slots, path_count[p]) : path_count[p];
       host_need = host_slots < path_count[p] ? (size_t)host_slots * nominal[p] : path_bytes[p];
+      if (host_sm) flag_devs[dst_dev] = 1;
     }
   }
-  ensure_arenas(ctx, stage_need, nc, host_need);
+  ensure_arenas(ctx, stage_need, flag_devs, nc, host_need);
 
   const uint64_t s0 = (uint64_t)(uintptr_t)src, d0 = (uint64_t)(uintptr_t)dst;
   std::vector<std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>> tiles(ctx->phys.size());
@@ -328,8 +342,7 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
     const int p = ch.path_index;
     const uint64_t round = (uint64_t)ch.seq;
     if (P.kind == MP_PATH_DIRECT) {
-      const bool sm = o.direct_engine == MP_ENGINE_SM && size >= (uint64_t)o.sm_min_bytes;
-      if (sm) {
+      if (direct_sm) {
         int exec = o.pull ? dp : sp;
         mpk::Tile proto{};
         uint64_t tile = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[exec].sms);
@@ -343,8 +356,7 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
       const int rp = L.phys;
       uint8_t* stage = L.stage + stage_off[p];
       stage_off[p] += ch.length;
-      const bool sm = o.relay_engine == MP_ENGINE_SM && size >= (uint64_t)o.sm_min_bytes;
-      if (sm) {
+      if (relay_sm) {
         uint64_t t1 = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[sp].sms);
         uint64_t t2 = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[rp].sms);
         uint32_t n1 = (uint32_t)ntiles_of(ch.length, t1), n2 = (uint32_t)ntiles_of(ch.length, t2);
@@ -365,6 +377,28 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
         e->ce.push_back(CeOp{sp, lane_base[p], stage, (const uint8_t*)src + ch.offset, (size_t)ch.length, -1, ev});
         e->ce.push_back(CeOp{rp, lane_base[p] + 1, (uint8_t*)dst + ch.offset, stage, (size_t)ch.length, ev, -1});
       }
+    } else if (host_sm) {
+      // host-staged by the SM kernels: hop1 tiles (src device) bulk-store into
+      // mapped pinned memory over PCIe, hop2 tiles (dst device) bulk-load it
+      // back after the chunk's flag (in dst memory) counts every hop1 tile.
+      Logi& L = ctx->logi[dst_dev];
+      uint8_t* host_dev = nullptr;
+      CK(cudaHostGetDevicePointer((void**)&host_dev, ctx->host_stage, 0));
+      uint8_t* slot = host_dev + stage_off[p];
+      stage_off[p] += ch.length;
+      const uint64_t th = std::min<uint64_t>(auto_tile_bytes(ctx, path_bytes[p], ctx->phys[sp].sms),
+                                             kHostTileBytes);
+      uint32_t n1 = (uint32_t)ntiles_of(ch.length, th), n2 = n1;
+      mpk::Tile h1{};
+      h1.signal = L.flags + c;
+      append_tiles(tiles[sp], 2 * round, s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
+      mpk::Tile h2{};
+      h2.wait = L.flags + c;
+      h2.pass = L.flags + L.flag_cap + c;
+      h2.wait_count = n1;
+      h2.pass_count = n2;
+      h2.flags = mpk::TILE_SRC_MUTABLE;
+      append_tiles(tiles[dp], 2 * round + 3, (uint64_t)(uintptr_t)slot, d0 + ch.offset, ch.length, th, h2);
     } else {  // host-staged: D2H into pinned staging, H2D out of it (copy engines)
       int seq = ch.seq;
       host_chunk_of_seq.push_back(c);
@@ -532,6 +566,9 @@ int mp_ctx_create(int32_t n_logical, const int32_t* device_map, mp_ctx** out) {
   ctx->opts.host_slots = 0;
   ctx->opts.pull = 0;
   ctx->opts.sm_min_bytes = 0;
+  // copy engines move the host-staged path: SM bulk copies to/from mapped
+  // pinned memory measured ~10x slower (profiles/r01_exp_host.jsonl)
+  ctx->opts.host_engine = MP_ENGINE_CE;
   ctx->opts.unroll = 8;
   ctx->opts.tma_stages = 4;
   ctx->opts.tma_block = 32768;
@@ -638,7 +675,8 @@ int mp_ctx_set_engine(mp_ctx* ctx, const mp_engine_opts* o) {
   if (o->tma_stages < 2 || o->tma_stages > 16) return fail(MP_ERR_VALUE, "tma_stages must be in [2, 16]");
   if (o->tma_block < 16 || o->tma_block % 16 || (int64_t)o->tma_block * o->tma_stages > 227 * 1024)
     return fail(MP_ERR_VALUE, "tma_block must be a multiple of 16 with stages*block <= 227 KiB");
-  if (o->direct_engine < 0 || o->direct_engine > 1 || o->relay_engine < 0 || o->relay_engine > 1)
+  if (o->direct_engine < 0 || o->direct_engine > 1 || o->relay_engine < 0 || o->relay_engine > 1 ||
+      o->host_engine < 0 || o->host_engine > 1)
     return fail(MP_ERR_VALUE, "unknown engine");
   std::lock_guard<std::mutex> lk(ctx->mu);
   clear_cache(ctx);

@@ -102,6 +102,7 @@ class Engine:
         self.topology = topology
 
     def configure(self, *, direct: str | None = None, relay: str | None = None,
+                  host: str | None = None,
                   ctas_per_sm: int | None = None, threads: int | None = None,
                   tile_bytes: int | None = None, host_slots: int | None = None,
                   pull: bool | None = None, sm_min_bytes: int | None = None,
@@ -122,6 +123,8 @@ class Engine:
             o.direct_engine = ENGINES[direct]
         if relay is not None:
             o.relay_engine = ENGINES[relay]
+        if host is not None:
+            o.host_engine = ENGINES[host]
         if ctas_per_sm is not None:
             o.ctas_per_sm = ctas_per_sm
         if threads is not None:

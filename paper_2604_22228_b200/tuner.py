@@ -1,0 +1,163 @@
+"""Measurement-driven configuration search (replaces the simulated tuner).
+
+Same interface as the reference's `mpsim.tuner` (tuner.py:29-124):
+GridPoint, default_grid, TuningEntry, TuningTable (nearest-size lookup, CSV
+round trip in the reference's schema) and `tune` — but every grid point is
+*timed on the GPU* through the engine (CUDA events around cached-graph
+replays or per-call stream launches) instead of being simulated.  Ties break
+as in the reference: fewer paths, then fewer chunks, then host off.
+
+`calibrate_host_bandwidth` closes the loop between measurement and the
+planner: the reference splits bytes purely by bottleneck bandwidth
+(paths.py:144-150), so the host link's entry in the `.topo` must be the rate
+the host-staged path actually sustains next to the direct path (pipeline
+fill, per-copy overhead, PCIe duplex contention) — found here by timing the
+real multi-path transfer for candidate values.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+from .paths import PathConfig
+from .topology import Topology, load_topology, mesh_text
+
+GRAPH_MODE = "graph"
+STREAMED_MODE = "streamed"
+DEFAULT_GPU_PATHS = (1, 2, 3)
+DEFAULT_HOST_FLAGS = (False, True)
+DEFAULT_MAX_CHUNKS = (1, 2, 4, 8, 16, 32)
+MODES = (GRAPH_MODE, STREAMED_MODE)
+
+
+@dataclass(frozen=True)
+class GridPoint:
+    gpu_paths: int
+    host: bool
+    max_chunks: int
+
+
+def default_grid(max_gpu_paths: int = 3) -> list[GridPoint]:
+    return [GridPoint(g, h, c)
+            for g in DEFAULT_GPU_PATHS if g <= max_gpu_paths
+            for h in DEFAULT_HOST_FLAGS
+            for c in DEFAULT_MAX_CHUNKS]
+
+
+@dataclass(frozen=True)
+class TuningEntry:
+    size: int
+    mode: str
+    best: GridPoint
+    makespan: float  # measured seconds per transfer at the winning point
+
+
+@dataclass
+class TuningTable:
+    topology: str
+    entries: list[TuningEntry]
+
+    def lookup(self, size: int, mode: str) -> TuningEntry:
+        """Entry of the nearest tuned size (log distance; the smaller size wins ties)."""
+        cands = [e for e in self.entries if e.mode == mode]
+        if not cands:
+            raise KeyError(f"no tuning entries for mode {mode!r}")
+        return min(cands, key=lambda e: (abs(math.log(size) - math.log(e.size)), e.size))
+
+    def config_for(self, size: int, mode: str = GRAPH_MODE,
+                   base: PathConfig | None = None) -> PathConfig:
+        p = self.lookup(size, mode).best
+        b = base or PathConfig()
+        return PathConfig(p.gpu_paths, p.host, p.max_chunks, mode == GRAPH_MODE,
+                          b.cache_capacity, b.share_policy)
+
+    def to_csv(self) -> str:
+        lines = ["size,mode,gpu_paths,host,max_chunks,makespan"]
+        for e in self.entries:
+            lines.append(f"{e.size},{e.mode},{e.best.gpu_paths},"
+                         f"{'on' if e.best.host else 'off'},{e.best.max_chunks},{e.makespan!r}")
+        return "\n".join(lines) + "\n"
+
+    @classmethod
+    def from_csv(cls, text: str, topology: str = "") -> "TuningTable":
+        entries = []
+        for line in [ln for ln in text.splitlines() if ln.strip()][1:]:
+            size, mode, paths, host, chunks, makespan = line.split(",")
+            entries.append(TuningEntry(int(size), mode,
+                                       GridPoint(int(paths), host == "on", int(chunks)),
+                                       float(makespan)))
+        return cls(topology, entries)
+
+
+def measure_makespan(engine, config: PathConfig, size: int, src, dst, stream,
+                     reps: int = 10, warmup: int = 2) -> float:
+    """Seconds per transfer: CUDA events around `reps` back-to-back sends."""
+    import torch
+    for _ in range(warmup):
+        engine.send(src, dst, size, config, stream=stream, src_dev=0, dst_dev=1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        engine.send(src, dst, size, config, stream=stream, src_dev=0, dst_dev=1)
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / reps
+
+
+def tune(engine, sizes: list[int], grid: list[GridPoint] | None = None,
+         modes: tuple[str, ...] = MODES, reps: int = 10, device=None) -> TuningTable:
+    """Time every grid point per (size, mode) on the GPU; record the argmin."""
+    import torch
+    if not sizes:
+        raise ValueError("size list is empty")
+    n = len(engine.topology.accelerators)
+    grid = default_grid(n - 1) if grid is None else grid
+    if not grid:
+        raise ValueError("tuning grid is empty")
+    dev = device if device is not None else engine.device_map[0]
+    big = torch.empty(max(sizes), dtype=torch.uint8, device=f"cuda:{dev}")
+    out = torch.empty_like(big)
+    stream = torch.cuda.Stream(device=dev)
+    entries = []
+    for size in sizes:
+        for mode in modes:
+            best_key, best = None, None
+            for p in grid:
+                if p.gpu_paths > n - 1:
+                    continue
+                cfg = PathConfig(p.gpu_paths, p.host, p.max_chunks, mode == GRAPH_MODE)
+                t = measure_makespan(engine, cfg, size, big[:size], out[:size], stream, reps)
+                key = (t, p.gpu_paths, p.max_chunks, p.host)
+                if best_key is None or key < best_key:
+                    best_key, best = key, TuningEntry(size, mode, p, t)
+            entries.append(best)
+    engine.clear_cache()
+    return TuningTable(engine.topology.name, entries)
+
+
+def calibrate_host_bandwidth(engine, link_bw: float, size: int, max_chunks: int,
+                             candidates: list[float] | None = None, reps: int = 10,
+                             name: str = "calibrated") -> tuple[float, Topology, list]:
+    """Pick the host-link bandwidth for the `.topo` that maximises the measured
+    direct+host throughput at `size`; returns (host_bw, topology, trials)."""
+    import torch
+    n = len(engine.topology.accelerators)
+    if candidates is None:
+        candidates = [b * 1e9 for b in (1, 2, 4, 6, 8, 10, 12, 16, 20, 28, 40, 55)]
+    dev = engine.device_map[0]
+    src = torch.empty(size, dtype=torch.uint8, device=f"cuda:{dev}")
+    dst = torch.empty_like(src)
+    stream = torch.cuda.Stream(device=dev)
+    cfg = PathConfig(1, True, max_chunks, True)
+    trials = []
+    best = None
+    for bw in candidates:
+        topo = load_topology(mesh_text(name, n, link_bw, 1, 2e-6, bw, 1e-5, "full"))
+        engine.set_topology(topo)
+        t = measure_makespan(engine, cfg, size, src, dst, stream, reps)
+        trials.append((bw, size / t / 1e9))
+        if best is None or t < best[0]:
+            best = (t, bw, topo)
+    engine.set_topology(best[2])
+    return best[1], best[2], trials

@@ -1,11 +1,13 @@
 #!/bin/bash
-# tests + bench + ncu evidence in one gpurun call
+# tests + smoke + bench + ncu evidence in one gpurun call
 mkdir -p gpurun_out
 python paper_2604_22228_b200/build.py > gpurun_out/build.log 2>&1
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 tail -3 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --quick --steps 3 --warmup 3 > gpurun_out/ncu_launch_bench.log 2>&1; echo "ncu launches rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:transfer_kernel -s 6 -c 1 -o gpurun_out/transfer_full python bench.py --quick --steps 3 --warmup 3 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
-ls -la gpurun_out
+timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "bench ref rc=$?"
+export PROF_HOST_BW=${PROF_HOST_BW:-10e9}
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:transfer_kernel -s 2 -c 1 -o gpurun_out/transfer_512m python tools/prof_kernel.py > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_prof.csv python tools/prof_kernel.py > /dev/null 2>&1; echo "ncu list rc=$?"
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench.csv python bench.py --quick --steps 3 --warmup 3 > gpurun_out/ncu_bench.log 2>&1; echo "ncu bench list rc=$?"
