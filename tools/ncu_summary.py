@@ -25,7 +25,8 @@ KEYS = {
     "lts__t_bytes.sum": "l2_bytes",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
 }
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Kbyte/block": 1e3, "ns": 1e-9,
+         "us": 1e-6, "ms": 1e-3, "nsecond": 1e-9, "usecond": 1e-6,
          "msecond": 1e-3, "second": 1}
 
 
