@@ -7,10 +7,12 @@ loopback — logical GPU0 and GPU1 of the topology both map to cuda:0.  The
 direct path is then an HBM->HBM copy by the SM transfer kernel and the
 host-staged path a real D2H + H2D over PCIe Gen5 through pinned memory; the
 planner, graph cache and engine are exactly the multi-GPU ones.
-A step = one message of --size bytes (default 512 MiB, larger than L2, so no
-L2 flush is needed) sent with the cached CUDA graph.  `value` is S*K / device
-time of K steps; `e2e` adds the H2D of the source from pinned host memory
-and the D2H of the delivered buffer to every step, through the public API.
+A step = one osu_bw window: --window (64) back-to-back messages of --size
+bytes (default 512 MiB, larger than L2, so no L2 flush is needed) sent with
+the cached CUDA graph.  `value` is K*W*S / device time of K steps; `e2e`
+times the same send through the public API per message with the H2D of the
+message from pinned host memory (double-buffered) and the D2H of the step's
+result (an int64 checksum of the delivered buffer) inside the region.
 
 --impl reference: the reference's CPU implementation of the path — the
 oracle restatement (oracle/transfer.py, the reference package itself never
@@ -44,7 +46,7 @@ def parse():
     ap.add_argument("--size", type=int, default=512 * MiB)
     ap.add_argument("--chunks", type=int, default=8)
     ap.add_argument("--no-sweep", action="store_true")
-    ap.add_argument("--window", type=int, default=16)
+    ap.add_argument("--window", type=int, default=64, help="messages per step (osu_bw window)")
     ap.add_argument("--quick", action="store_true",
                     help="headline only: no sweep, lifecycle or CPU baseline (for ncu)")
     return ap.parse_args()
@@ -73,6 +75,27 @@ class Clocks:
         self._t = threading.Thread(target=self._run, daemon=True)
 
     def _run(self):
+        try:  # NVML directly: ~0.1 ms per sample instead of ~200 ms per nvidia-smi call
+            import pynvml as nv
+            nv.nvmlInit()
+            try:  # the CUDA ordinal's own GPU, by PCI address (CUDA_VISIBLE_DEVICES-proof)
+                import torch
+                p = torch.cuda.get_device_properties(self.index)
+                h = nv.nvmlDeviceGetHandleByPciBusId(
+                    f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0")
+            except Exception:
+                h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            while not self._stop.is_set():
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), str(mx)]
+                                    + ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.01)
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index),
@@ -190,7 +213,8 @@ def workload_config(args):
                         f"multi-path, max_chunks {args.chunks}, cached CUDA-graph replay; N=1: "
                         "logical GPU0/GPU1 both on cuda:0 (loopback: direct = HBM copy, "
                         "host = PCIe Gen5 D2H+H2D)",
-            "msg_bytes": args.size, "max_chunks": args.chunks, "paths": "direct+host",
+            "msg_bytes": args.size, "window": args.window, "max_chunks": args.chunks,
+            "paths": "direct+host",
             "l2": "inputs larger than L2 (512 MiB > 126 MB)", "parallelism": f"n{args.gpus}"}
 
 
@@ -280,8 +304,10 @@ def run_ours(args, rank, world):
     direct_bytes = sum(c[2] for c in ochunks if c[0] == 0)
     host_bytes = size - direct_bytes
 
-    # 2. headline: K steps of cached-graph replay, device time, clocks sampled
-    for _ in range(args.warmup):
+    # 2. headline: K steps, each one osu_bw window of W back-to-back messages
+    #    (cached-graph replay), device time, clocks sampled during the region
+    W = args.window
+    for _ in range(args.warmup * W):
         eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
     torch.cuda.synchronize()
     if world > 1:
@@ -289,7 +315,7 @@ def run_ours(args, rank, world):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(dev) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(args.steps * W):
             eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -299,9 +325,9 @@ def run_ours(args, rank, world):
         tt = torch.tensor([t], device=f"cuda:{dev}")
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         t = float(tt)
-    value = world * args.steps * size / t / 1e9
+    value = world * args.steps * W * size / t / 1e9
     single_t = time_sends(torch, eng, PathConfig(max_chunks=1, graph_mode=True), src, dst,
-                          size, args.steps, 3, stream)
+                          size, args.steps * 4, 3, stream)
 
     # 3. dominant kernel: transfer_kernel duration (events on its stream, streamed mode)
     cfg_s = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=args.chunks,
@@ -319,24 +345,38 @@ def run_ours(args, rank, world):
 
     # 4. e2e through the public API: H2D of the message from pinned host memory,
     #    the multi-path send, and a D2H of the step's result (a device checksum)
+    #    Double-buffered: the H2D of message i+1 (copy stream) overlaps the
+    #    send + checksum of message i; every step still moves its own bytes.
     hsrc = torch.empty(size, dtype=torch.uint8, pin_memory=True)
     hsum = torch.empty(1, dtype=torch.int64, pin_memory=True)
     hsrc.copy_(src.cpu())
     want = int(src.sum(dtype=torch.int64))
-    e2e_steps = max(3, args.steps // 4)
+    e2e_steps = max(4, args.steps // 2)
     cur = torch.cuda.current_stream()
+    cs = torch.cuda.Stream(device=dev)
+    bufs = [src, torch.empty_like(src)]
+    landed = [torch.cuda.Event() for _ in range(2)]
+    consumed = [torch.cuda.Event() for _ in range(2)]
+    for ev in consumed:
+        ev.record(cur)
 
-    def e2e_step():
-        src.copy_(hsrc, non_blocking=True)
-        eng.send(src, dst, size, cfg, src_dev=0, dst_dev=1)
-        hsum.copy_(dst.sum(dtype=torch.int64).view(1), non_blocking=True)
-    for _ in range(2):
-        e2e_step()
+    def e2e_run(n):
+        for i in range(n):
+            b = i % 2
+            with torch.cuda.stream(cs):
+                cs.wait_event(consumed[b])          # send i-2 finished reading this buffer
+                bufs[b].copy_(hsrc, non_blocking=True)
+                landed[b].record(cs)
+            cur.wait_event(landed[b])
+            eng.send(bufs[b], dst, size, cfg, stream=cur, src_dev=0, dst_dev=1)
+            consumed[b].record(cur)
+            hsum.copy_(dst.sum(dtype=torch.int64).view(1), non_blocking=True)
+    e2e_run(2)
     torch.cuda.synchronize()
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     c0.record(cur)
-    for _ in range(e2e_steps):
-        e2e_step()
+    cs.wait_event(c0)
+    e2e_run(e2e_steps)
     c1.record(cur)
     torch.cuda.synchronize()
     e2e = e2e_steps * size / (c0.elapsed_time(c1) / 1e3) / 1e9
@@ -379,7 +419,7 @@ def run_ours(args, rank, world):
         "reference_cpu_path_us": ref_cpu,
         "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": size,
                 "d2h_bytes_per_step": 8, "result": "int64 checksum of the delivered buffer"},
-        "gpu_launches": args.steps * st.kernels,
+        "gpu_launches": args.steps * W * st.kernels,
         "clocks": clk.summary(),
         "graph": {"nodes_logical": st.nodes_logical, "nodes_physical": st.nodes_physical,
                   "kernels_per_send": st.kernels, "ce_copies_per_send": st.ce_copies,
@@ -399,11 +439,16 @@ def run_sweep(torch, eng, topo_text, dev, stream):
     direct+host multi-path with the graph cache on / off, and the measured
     tuner's best configuration."""
     from paper_2604_22228_b200 import Engine, PathConfig, load_topology
-    from paper_2604_22228_b200.tuner import GridPoint, tune
+    from paper_2604_22228_b200.tuner import GridPoint, tune, tune_engines
     ce = Engine(load_topology(topo_text), [dev, dev])
     ce.configure(direct="ce")
+    # measured per-size choices: direct mechanism (SM kernel vs CE), then the
+    # reference tuner's grid (paths x host x chunks) on top of it
+    auto = Engine(load_topology(topo_text), [dev, dev])
+    rules, _ = tune_engines(auto, SWEEP_SIZES, reps=5)
+    auto.set_size_policy(rules)
     grid = [GridPoint(1, h, c) for h in (False, True) for c in (1, 2, 4, 8, 16, 32)]
-    table = tune(eng, SWEEP_SIZES, grid, modes=("graph",), reps=5)
+    table = tune(auto, SWEEP_SIZES, grid, modes=("graph",), reps=5)
     rows = []
     big = torch.empty(SWEEP_SIZES[-1], dtype=torch.uint8, device=f"cuda:{dev}")
     out = torch.empty_like(big)
@@ -419,12 +464,14 @@ def run_sweep(torch, eng, topo_text, dev, stream):
         for name, e, cfg in arms:
             row[name] = size / time_sends(torch, e, cfg, src, dst, size, steps, warm, stream) / 1e9
         best = table.lookup(size, "graph").best
-        row["tuned"] = size / time_sends(torch, eng, table.config_for(size), src, dst, size,
+        row["tuned"] = size / time_sends(torch, auto, table.config_for(size), src, dst, size,
                                          steps, warm, stream) / 1e9
-        row["tuned_point"] = [best.gpu_paths, best.host, best.max_chunks]
+        row["tuned_point"] = [best.gpu_paths, best.host, best.max_chunks,
+                              next(e for b, e in rules if size <= b)]
         rows.append(row)
     ce.close()
-    return rows, table.to_csv()
+    auto.close()
+    return rows, {"table_csv": table.to_csv(), "direct_engine_policy": rules}
 
 
 def run_lifecycle(torch, eng, dev, stream):

@@ -46,7 +46,7 @@ namespace {
       throw Error{MP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)};     \
   } while (0)
 
-using KernelFn = void (*)(const mpk::Tile*, unsigned, mpk::Ctl*, unsigned, unsigned);
+using KernelFn = void (*)(const mpk::Tile*, unsigned, mpk::Ctl*, unsigned, unsigned, unsigned);
 
 KernelFn pick_kernel(const mp_engine_opts& o) {
   if (o.copy_kind == MP_COPY_TMA) return mpk::transfer_kernel<1, 8>;
@@ -62,12 +62,15 @@ size_t kernel_smem(const mp_engine_opts& o) {
 }
 
 // Launch the persistent transfer kernel (mp_kernels.cuh) over one tile table.
+// `nstatic` > 0 only for tables without flag waits: static first tiles must
+// never be waited on by another CTA (residency of every CTA is not guaranteed).
 void launch_transfer(const mp_engine_opts& o, unsigned grid, cudaStream_t s, const mpk::Tile* tiles,
-                     unsigned ntiles, mpk::Ctl* ctl) {
+                     unsigned ntiles, mpk::Ctl* ctl, unsigned nstatic) {
   KernelFn fn = pick_kernel(o);
   size_t smem = kernel_smem(o);
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  fn<<<grid, o.threads, smem, s>>>(tiles, ntiles, ctl, (unsigned)o.tma_stages, (unsigned)o.tma_block);
+  fn<<<grid, o.threads, smem, s>>>(tiles, ntiles, ctl, (unsigned)o.tma_stages, (unsigned)o.tma_block,
+                                   nstatic);
   CK(cudaGetLastError());
 }
 
@@ -121,6 +124,7 @@ struct Program {
   mpk::Tile* d_tiles = nullptr;
   unsigned ntiles = 0;
   unsigned grid = 0;
+  unsigned nstatic = 0;  // = grid when the table has no flag waits
 };
 
 struct Entry {
@@ -157,6 +161,7 @@ struct mp_ctx {
   void* last_stream = nullptr;
   bool have_last = false;
   double kernel_ms = 0.0;
+  std::vector<std::pair<uint64_t, int>> size_policy;  // (max_bytes, direct engine)
   std::mutex mu;
 };
 
@@ -248,29 +253,51 @@ constexpr uint64_t kHostTileBytes = 64 << 10;
 
 uint64_t auto_tile_bytes(const mp_ctx* ctx, uint64_t path_bytes, int sms) {
   if (ctx->opts.tile_bytes > 0) return (uint64_t)ctx->opts.tile_bytes;
-  // aim for >= 4 tiles per resident CTA (tail balance), 16 .. 256 KiB, multiple
-  // of 4 KiB; 256 KiB tiles measured best for the 512 MiB copy (r01 sweep)
+  // aim for >= 12 tiles per resident CTA (the tail is at most one tile),
+  // 32 .. 256 KiB, multiple of 4 KiB; the TMA stream is continuous across
+  // tiles so small tiles cost only a claim + a prefetched descriptor
   uint64_t ctas = (uint64_t)sms * std::max(1, ctx->opts.ctas_per_sm);
-  uint64_t t = path_bytes / (ctas * 4);
-  t = std::max<uint64_t>(t, 16 << 10);
+  uint64_t t = path_bytes / (ctas * 12);
+  t = std::max<uint64_t>(t, 32 << 10);
   t = std::min<uint64_t>(t, 256 << 10);
   return (t + 4095) & ~(uint64_t)4095;
+}
+
+// Interior tile boundaries of [0, len): every `tile` bytes, moved down to a
+// 16-byte-aligned destination address so only a chunk's first and last tiles
+// carry an unaligned head/tail (chunk offsets are mostly unaligned,
+// pipeline.py:66-77).
+std::vector<uint64_t> tile_cuts(uint64_t dst, uint64_t len, uint64_t tile) {
+  std::vector<uint64_t> cuts{0};
+  uint64_t o = 0;
+  while (len - o > tile) {
+    uint64_t next = o + tile;
+    uint64_t adj = next - ((dst + next) & 15u);
+    if (adj > o) next = adj;
+    cuts.push_back(next);
+    o = next;
+  }
+  cuts.push_back(len);
+  return cuts;
 }
 
 // Split [src, src+len) -> dst into tiles appended to `out`.
 void append_tiles(std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>& out,
                   uint64_t order, uint64_t src, uint64_t dst, uint64_t len, uint64_t tile,
                   const mpk::Tile& proto) {
-  for (uint64_t o = 0; o < len; o += tile) {
+  auto cuts = tile_cuts(dst, len, tile);
+  for (size_t i = 0; i + 1 < cuts.size(); ++i) {
     mpk::Tile t = proto;
-    t.src = src + o;
-    t.dst = dst + o;
-    t.len = std::min(tile, len - o);
+    t.src = src + cuts[i];
+    t.dst = dst + cuts[i];
+    t.len = cuts[i + 1] - cuts[i];
     out.push_back({{order, out.size()}, t});
   }
 }
 
-uint64_t ntiles_of(uint64_t len, uint64_t tile) { return (len + tile - 1) / tile; }
+uint64_t ntiles_of(uint64_t dst, uint64_t len, uint64_t tile) {
+  return tile_cuts(dst, len, tile).size() - 1;
+}
 
 // Lower a chunk plan to device programs and copy-engine ops.
 Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* dst, uint64_t size,
@@ -296,7 +323,13 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
   }
   // engines per path type for this message size (measured thresholds)
   const bool sm_ok = size >= (uint64_t)o.sm_min_bytes;
-  const bool direct_sm = o.direct_engine == MP_ENGINE_SM && sm_ok;
+  int direct_engine = o.direct_engine;
+  for (const auto& rule : ctx->size_policy)
+    if (size <= rule.first) {
+      direct_engine = rule.second;
+      break;
+    }
+  const bool direct_sm = direct_engine == MP_ENGINE_SM && sm_ok;
   const bool relay_sm = o.relay_engine == MP_ENGINE_SM && sm_ok;
   const bool host_sm = o.host_engine == MP_ENGINE_SM && sm_ok;
   // staging requirements
@@ -306,13 +339,14 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
   int host_slots = 0;
   for (int p = 0; p < np; ++p) {
     if (e->paths[p].kind == MP_PATH_GPU) {
-      stage_need[e->paths[p].stage] = path_bytes[p];
+      stage_need[e->paths[p].stage] = path_bytes[p] + 16 * (size_t)path_count[p];
       if (relay_sm) flag_devs[e->paths[p].stage] = 1;
     }
     if (e->paths[p].kind == MP_PATH_HOST) {
       // the SM host path keeps every chunk resident (its share is a few MB)
       host_slots = (o.host_slots > 0 && !host_sm) ? std::min(o.host_slots, path_count[p]) : path_count[p];
-      host_need = host_slots < path_count[p] ? (size_t)host_slots * nominal[p] : path_bytes[p];
+      host_need = host_slots < path_count[p] ? (size_t)host_slots * nominal[p]
+                                              : path_bytes[p] + 16 * (size_t)path_count[p];
       if (host_sm) flag_devs[dst_dev] = 1;
     }
   }
@@ -354,12 +388,15 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
     } else if (P.kind == MP_PATH_GPU) {
       Logi& L = ctx->logi[P.stage];
       const int rp = L.phys;
+      // staging offset congruent to the source mod 16 keeps hop1 on the TMA path
+      stage_off[p] += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)L.stage + stage_off[p])) & 15u;
       uint8_t* stage = L.stage + stage_off[p];
       stage_off[p] += ch.length;
       if (relay_sm) {
         uint64_t t1 = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[sp].sms);
         uint64_t t2 = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[rp].sms);
-        uint32_t n1 = (uint32_t)ntiles_of(ch.length, t1), n2 = (uint32_t)ntiles_of(ch.length, t2);
+        uint32_t n1 = (uint32_t)ntiles_of((uint64_t)(uintptr_t)stage, ch.length, t1);
+        uint32_t n2 = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, t2);
         mpk::Tile h1{};
         h1.signal = L.flags + c;
         append_tiles(tiles[sp], 2 * round, s0 + ch.offset, (uint64_t)(uintptr_t)stage, ch.length, t1, h1);
@@ -384,11 +421,13 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
       Logi& L = ctx->logi[dst_dev];
       uint8_t* host_dev = nullptr;
       CK(cudaHostGetDevicePointer((void**)&host_dev, ctx->host_stage, 0));
+      stage_off[p] += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)host_dev + stage_off[p])) & 15u;
       uint8_t* slot = host_dev + stage_off[p];
       stage_off[p] += ch.length;
       const uint64_t th = std::min<uint64_t>(auto_tile_bytes(ctx, path_bytes[p], ctx->phys[sp].sms),
                                              kHostTileBytes);
-      uint32_t n1 = (uint32_t)ntiles_of(ch.length, th), n2 = n1;
+      uint32_t n1 = (uint32_t)ntiles_of((uint64_t)(uintptr_t)slot, ch.length, th);
+      uint32_t n2 = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, th);
       mpk::Tile h1{};
       h1.signal = L.flags + c;
       append_tiles(tiles[sp], 2 * round, s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
@@ -436,6 +475,9 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
     pr.ntiles = (unsigned)flat.size();
     Phys& P = ctx->phys[ph];
     pr.grid = (unsigned)std::min<uint64_t>(flat.size(), (uint64_t)P.sms * std::max(1, o.ctas_per_sm));
+    bool waits = false;
+    for (const auto& t : flat) waits |= t.wait != nullptr;
+    pr.nstatic = waits ? 0u : pr.grid;
     CK(cudaSetDevice(P.ordinal));
     CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile)));
     CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
@@ -466,7 +508,7 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing) {
     CK(cudaSetDevice(P.ordinal));
     bool t = timing && pr.phys == e->src_phys;
     if (t) CK(cudaEventRecord(P.kt0, P.kstream));
-    launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl);
+    launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic);
     if (t) CK(cudaEventRecord(P.kt1, P.kstream));
   }
   // copy-engine lanes
@@ -685,6 +727,27 @@ int mp_ctx_set_engine(mp_ctx* ctx, const mp_engine_opts* o) {
   GUARD_END
 }
 
+int mp_ctx_set_size_policy(mp_ctx* ctx, const uint64_t* max_bytes, const int32_t* direct_engine,
+                           int32_t n) {
+  GUARD_BEGIN
+  if (!ctx || n < 0 || (n > 0 && (!max_bytes || !direct_engine)))
+    return fail(MP_ERR_VALUE, "bad size policy arguments");
+  std::vector<std::pair<uint64_t, int>> rules;
+  for (int i = 0; i < n; ++i) {
+    if (direct_engine[i] != MP_ENGINE_SM && direct_engine[i] != MP_ENGINE_CE)
+      return fail(MP_ERR_VALUE, "unknown engine in size policy");
+    if (i > 0 && max_bytes[i] <= max_bytes[i - 1])
+      return fail(MP_ERR_VALUE, "size policy bounds must increase");
+    rules.emplace_back(max_bytes[i], direct_engine[i]);
+  }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g;
+  clear_cache(ctx);
+  ctx->size_policy = rules;
+  return MP_OK;
+  GUARD_END
+}
+
 int mp_ctx_get_engine(const mp_ctx* ctx, mp_engine_opts* o) {
   if (!ctx || !o) return fail(MP_ERR_VALUE, "null argument");
   *o = ctx->opts;
@@ -896,7 +959,7 @@ int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t byt
   CK(cudaMemcpy(dt, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
   unsigned grid = (unsigned)std::min<uint64_t>(flat.size(), (uint64_t)S.sms * ctx->opts.ctas_per_sm);
   out_gbps[0] = time_it(S, [&](cudaStream_t s) {
-    launch_transfer(ctx->opts, grid, s, dt, (unsigned)flat.size(), S.ctl);
+    launch_transfer(ctx->opts, grid, s, dt, (unsigned)flat.size(), S.ctl, grid);
   });
   out_gbps[1] = time_it(S, [&](cudaStream_t s) { cudaMemcpyAsync(h, a, bytes, cudaMemcpyDeviceToHost, s); });
   out_gbps[2] = time_it(D, [&](cudaStream_t s) { cudaMemcpyAsync(b, h, bytes, cudaMemcpyHostToDevice, s); });

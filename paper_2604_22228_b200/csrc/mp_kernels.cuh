@@ -190,121 +190,243 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Thread 0 streams `len` bytes (16-byte aligned, multiple of 16) through the ring.
-__device__ __forceinline__ void tma_stream(TmaRing& r, const uint8_t* src, uint8_t* dst, uint64_t len) {
-  const uint64_t nblk = (len + r.block - 1) / r.block;
-  auto bytes_of = [&](uint64_t b) -> uint32_t {
-    uint64_t rem = len - b * r.block;
-    return (uint32_t)(rem < r.block ? rem : r.block);
-  };
-  auto load = [&](uint64_t b) {
-    uint32_t s = (uint32_t)(b % r.stages);
-    uint32_t n = bytes_of(b);
-    mbar_expect_tx(&r.bar[s], n);
-    tma_load(r.buf + (size_t)s * r.block, src + b * r.block, n, &r.bar[s]);
-  };
-  const uint64_t pro = nblk < r.stages ? nblk : r.stages;
-  for (uint64_t b = 0; b < pro; ++b) load(b);
-  for (uint64_t b = 0; b < nblk; ++b) {
-    uint32_t s = (uint32_t)(b % r.stages);
-    mbar_wait(&r.bar[s], (r.phase >> s) & 1u);
-    r.phase ^= 1u << s;
-    tma_store(dst + b * r.block, r.buf + (size_t)s * r.block, bytes_of(b));
-    bulk_commit();
-    // refill the stage of block b-1 once its store has read shared memory
-    if (b >= 1 && b - 1 + r.stages < nblk) {
-      bulk_wait_read<1>();
-      load(b - 1 + r.stages);
+// Acquire-wait on a hop2 tile's flag; the last hop2 tile of the chunk to pass
+// re-arms flag and pass counter so a cached graph replays without a memset.
+__device__ __forceinline__ void wait_tile_flag(const Tile& t, Ctl* ctl) {
+  const uint64_t t0 = globaltimer();
+  while (ld_acquire_sys(t.wait) < t.wait_count) {
+    if (globaltimer() - t0 > kWaitTimeoutNs) {
+      atomicExch(&ctl->error, 1u);
+      break;
     }
+    __nanosleep(64);
   }
-  bulk_wait_read<0>();  // ring free for the next tile
+  if (atomicAdd(t.pass, 1u) + 1u == t.pass_count) {
+    *(volatile uint32_t*)t.pass = 0u;
+    *(volatile uint32_t*)t.wait = 0u;
+  }
 }
 
-template <bool MUTABLE>
-__device__ __forceinline__ void copy_range_tma(TmaRing& r, const uint8_t* src, uint8_t* dst,
-                                               uint64_t len) {
-  const unsigned tid = threadIdx.x;
-  uint64_t head = (16u - ((uintptr_t)dst & 15u)) & 15u;
-  if (head > len) head = len;
-  const uint64_t body = (len - head) & ~(uint64_t)15;
-  const uint64_t tail_at = head + body;
-  if (tid == 0) {
-    if (body) {
-      if (MUTABLE) fence_proxy_async();  // staged bytes were written by the generic proxy
-      tma_stream(r, src + head, dst + head, body);
-    }
-  } else if (tid >= 32) {
-    const unsigned k = tid - 32;
-    if (k < head) dst[k] = MUTABLE ? *(volatile const uint8_t*)(src + k) : src[k];
-    if (k < len - tail_at)
-      dst[tail_at + k] = MUTABLE ? *(volatile const uint8_t*)(src + tail_at + k) : src[tail_at + k];
-  }
+__device__ __forceinline__ void release_signal(uint32_t* sig) {
+  __threadfence_system();
+  red_release_sys_add(sig, 1u);
 }
+
+// Per-stage bookkeeping of the TMA block stream.
+struct BlockMeta {
+  uint8_t* dst;
+  uint32_t bytes;
+  uint32_t* signal;  // set on the last block of a hop1 tile
+};
+
+// The TMA engine: thread 0 streams 16-byte-aligned tile bodies through the
+// shared-memory ring as ONE continuous block sequence that spans tiles, so the
+// ring stays full across tile boundaries (no per-tile drain).  Loads run up to
+// `stages` blocks ahead of stores; stage s is refilled once the store that
+// last used it has read shared memory (bulk-group .read completion, lagging
+// one store).  Tiles that must wait on a relay flag, or whose src/dst disagree
+// mod 16, drain the stream first (a waited-on hop1 tile may be one this CTA
+// still holds); misaligned tiles are handed back to the whole CTA.
+// Returns 0 when the tile table is exhausted, 1 with *coop = a tile for the CTA.
+struct TmaEngine {
+  TmaRing r;
+  BlockMeta* meta;
+  const Tile* tiles;
+  unsigned ntiles;
+  Ctl* ctl;
+  unsigned next_claim;
+  // loader cursor
+  const uint8_t* ls = nullptr;
+  uint8_t* ld = nullptr;
+  uint64_t lrem = 0;
+  uint32_t* lsig = nullptr;
+  int blocked = -1;  // -1 none, 0 table exhausted, 1 misaligned tile, 2 flag wait
+  Tile pending;
+  uint64_t g_load = 0, g_store = 0;
+
+  __device__ void start_tile(const Tile& t) {
+    const uint8_t* src = (const uint8_t*)t.src;
+    uint8_t* dst = (uint8_t*)t.dst;
+    const bool mut = t.flags & TILE_SRC_MUTABLE;
+    uint64_t head = (16u - ((uintptr_t)dst & 15u)) & 15u;
+    if (head > t.len) head = t.len;
+    const uint64_t body = (t.len - head) & ~(uint64_t)15;
+    const uint64_t tail_at = head + body;
+    const uint64_t tail = t.len - tail_at;
+    if (head | tail) {  // < 16 + 16 bytes: issue every load before any store
+      uint8_t hb[15], tb[15];
+#pragma unroll
+      for (int k = 0; k < 15; ++k) {
+        if ((uint64_t)k < head) hb[k] = mut ? *(volatile const uint8_t*)(src + k) : src[k];
+        if ((uint64_t)k < tail)
+          tb[k] = mut ? *(volatile const uint8_t*)(src + tail_at + k) : src[tail_at + k];
+      }
+#pragma unroll
+      for (int k = 0; k < 15; ++k) {
+        if ((uint64_t)k < head) dst[k] = hb[k];
+        if ((uint64_t)k < tail) dst[tail_at + k] = tb[k];
+      }
+    }
+    if (body == 0) {
+      if (t.signal) release_signal(t.signal);
+      return;
+    }
+    if (mut) fence_proxy_async();  // staged bytes were written by the generic proxy
+    ls = src + head;
+    ld = dst + head;
+    lrem = body;
+    lsig = t.signal;
+  }
+
+  // Make the loader cursor non-empty; false when blocked.  Claims run two
+  // deep: when tile k starts, tile k+1's descriptor is already in registers
+  // (`ahead`, loaded at the previous fetch) and the atomic for k+2 is issued
+  // now but only consumed at the next fetch — neither latency is exposed.
+  Tile ahead;
+  unsigned claim2;
+  unsigned nstatic;  // tiles [0, nstatic) go to CTA blockIdx.x without a claim
+  __device__ unsigned claim() { return atomicAdd(&ctl->work, 1u) + nstatic; }
+  __device__ void prime() {
+    next_claim = blockIdx.x < nstatic ? blockIdx.x : claim();
+    claim2 = claim();
+    if (next_claim < ntiles) ahead = tiles[next_claim];
+  }
+  __device__ bool fetch() {
+    while (lrem == 0) {
+      if (blocked >= 0) return false;
+      const unsigned w = next_claim;
+      if (w >= ntiles) {
+        blocked = 0;
+        return false;
+      }
+      const Tile t = ahead;
+      next_claim = claim2;
+      claim2 = next_claim < ntiles ? claim() : ntiles;
+      if (next_claim < ntiles) ahead = tiles[next_claim];
+      const bool aligned = (((uintptr_t)t.src ^ (uintptr_t)t.dst) & 15u) == 0;
+      if (t.wait || !aligned) {
+        pending = t;
+        blocked = t.wait ? 2 : 1;
+        return false;
+      }
+      start_tile(t);
+    }
+    return true;
+  }
+
+  __device__ bool issue_load() {
+    if (!fetch()) return false;
+    const uint32_t n = (uint32_t)(lrem < r.block ? lrem : r.block);
+    const uint32_t s = (uint32_t)(g_load % r.stages);
+    meta[s] = BlockMeta{ld, n, lrem == n ? lsig : nullptr};
+    mbar_expect_tx(&r.bar[s], n);
+    tma_load(r.buf + (size_t)s * r.block, ls, n, &r.bar[s]);
+    ls += n;
+    ld += n;
+    lrem -= n;
+    ++g_load;
+    return true;
+  }
+
+  __device__ int run(Tile* coop) {
+    for (;;) {
+      const uint64_t seg = g_store;  // every stage is free here
+      for (uint32_t i = 0; i < r.stages && issue_load(); ++i) {
+      }
+      while (g_store < g_load) {
+        const uint32_t s = (uint32_t)(g_store % r.stages);
+        mbar_wait(&r.bar[s], (r.phase >> s) & 1u);
+        r.phase ^= 1u << s;
+        tma_store(meta[s].dst, r.buf + (size_t)s * r.block, meta[s].bytes);
+        bulk_commit();
+        const uint64_t b = g_store++;
+        if (meta[s].signal) {  // hop1 tile complete: its bytes land before the release
+          bulk_wait_all();
+          fence_proxy_async();
+          release_signal(meta[s].signal);
+        }
+        if (b > seg) {  // refill the stage of block b-1 once its store has read smem
+          bulk_wait_read<1>();
+          issue_load();
+        }
+      }
+      bulk_wait_read<0>();
+      if (blocked == 0) return 0;
+      const Tile t = pending;
+      const int why = blocked;
+      blocked = -1;
+      if (t.wait) wait_tile_flag(t, ctl);
+      if (why == 1 || (((uintptr_t)t.src ^ (uintptr_t)t.dst) & 15u) != 0) {
+        *coop = t;
+        return 1;
+      }
+      start_tile(t);
+    }
+  }
+};
 
 template <int KIND, int UNROLL>
 __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ tiles,
                                                        unsigned ntiles, Ctl* ctl,
-                                                       unsigned stages, unsigned block) {
-  __shared__ unsigned s_claim[2];
+                                                       unsigned stages, unsigned block,
+                                                       unsigned nstatic) {
+  // Tiles [0, nstatic) (a prefix with no flag waits, nstatic <= gridDim.x) are
+  // taken by CTA blockIdx.x without a claim; the rest are claimed dynamically.
   __shared__ Tile s_tile;
+  __shared__ int s_cmd;
   __shared__ uint64_t s_bar[16];
+  __shared__ BlockMeta s_meta[16];
   extern __shared__ __align__(128) uint8_t s_ring[];
-  TmaRing ring{s_ring, s_bar, 0u, stages, block};
-  if (KIND == 1 && threadIdx.x == 0) {
-    for (unsigned s = 0; s < stages; ++s) mbar_init(&s_bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (threadIdx.x == 0) s_claim[0] = atomicAdd(&ctl->work, 1u);
-  __syncthreads();
-  unsigned w = s_claim[0];
-  unsigned parity = 1;
-  while (w < ntiles) {
+  if (KIND == 1) {
+    // ---- TMA: thread 0 streams; the CTA helps only with misaligned tiles ----
+    TmaEngine eng{TmaRing{s_ring, s_bar, 0u, stages, block}, s_meta, tiles, ntiles, ctl, 0u};
+    eng.nstatic = nstatic;
     if (threadIdx.x == 0) {
-      s_claim[parity] = atomicAdd(&ctl->work, 1u);  // prefetch the next claim
-      s_tile = tiles[w];
-      if (s_tile.wait) {
-        const uint64_t t0 = globaltimer();
-        while (ld_acquire_sys(s_tile.wait) < s_tile.wait_count) {
-          if (globaltimer() - t0 > kWaitTimeoutNs) {
-            atomicExch(&ctl->error, 1u);
-            break;
-          }
-          __nanosleep(64);
-        }
-        // last hop2 tile of the chunk to pass re-arms the flag for replay
-        if (atomicAdd(s_tile.pass, 1u) + 1u == s_tile.pass_count) {
-          *(volatile uint32_t*)s_tile.pass = 0u;
-          *(volatile uint32_t*)s_tile.wait = 0u;
-        }
-      }
+      for (unsigned s = 0; s < stages; ++s) mbar_init(&s_bar[s], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      eng.prime();
     }
+    for (;;) {
+      if (threadIdx.x == 0) s_cmd = eng.run(&s_tile);
+      __syncthreads();
+      if (s_cmd == 0) break;
+      const Tile& t = s_tile;
+      if (t.flags & TILE_SRC_MUTABLE)
+        copy_range<UNROLL, true>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
+      else
+        copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
+      __syncthreads();  // every thread's stores precede the release
+      if (threadIdx.x == 0 && t.signal) release_signal(t.signal);
+    }
+    if (threadIdx.x == 0) bulk_wait_all();
+  } else {
+    // ---- vector LDG/STG: the whole CTA copies each claimed tile ----
+    __shared__ unsigned s_claim[2];
+    if (threadIdx.x == 0)
+      s_claim[0] = blockIdx.x < nstatic ? blockIdx.x : atomicAdd(&ctl->work, 1u) + nstatic;
     __syncthreads();
-    const Tile& t = s_tile;
-    const bool mut = t.flags & TILE_SRC_MUTABLE;
-    const bool tma = KIND == 1 && ((((uintptr_t)t.src ^ (uintptr_t)t.dst) & 15u) == 0);
-    if (tma) {
-      if (mut) copy_range_tma<true>(ring, (const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
-      else copy_range_tma<false>(ring, (const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
-    } else if (mut) {
-      copy_range<UNROLL, true>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
-    } else {
-      copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
+    unsigned w = s_claim[0];
+    unsigned parity = 1;
+    while (w < ntiles) {
+      if (threadIdx.x == 0) {
+        s_claim[parity] = atomicAdd(&ctl->work, 1u) + nstatic;  // prefetch the next claim
+        s_tile = tiles[w];
+        if (s_tile.wait) wait_tile_flag(s_tile, ctl);
+      }
+      __syncthreads();
+      const Tile& t = s_tile;
+      if (t.flags & TILE_SRC_MUTABLE)
+        copy_range<UNROLL, true>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
+      else
+        copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
+      __syncthreads();  // every thread's stores precede the release below
+      if (threadIdx.x == 0 && t.signal) release_signal(t.signal);
+      w = s_claim[parity];
+      parity ^= 1u;
+      __syncthreads();  // s_tile / s_claim reuse
     }
-    if (tma && threadIdx.x == 0 && t.signal) {
-      bulk_wait_all();  // bulk stores complete before the release
-      fence_proxy_async();
-    }
-    __syncthreads();  // every thread's stores precede the release below
-    if (threadIdx.x == 0 && t.signal) {
-      __threadfence_system();
-      red_release_sys_add(t.signal, 1u);
-    }
-    w = s_claim[parity];
-    parity ^= 1u;
-    __syncthreads();  // s_tile / s_claim reuse
   }
   if (threadIdx.x == 0) {
-    if (KIND == 1) bulk_wait_all();
     __threadfence();
     if (atomicAdd(&ctl->exit, 1u) + 1u == gridDim.x) {  // last CTA re-arms the counters
       ctl->work = 0u;

@@ -139,6 +139,15 @@ class Engine:
             o.sm_min_bytes = sm_min_bytes
         check(lib.mp_ctx_set_engine(self._ctx, C.byref(o)))
 
+    def set_size_policy(self, rules: list[tuple[int, str]]) -> None:
+        """[(max_bytes, "sm"|"ce"), ...] increasing: the direct-path mechanism
+        per message size (from `tuner.tune_engines`); [] restores the default."""
+        n = len(rules)
+        mx = (C.c_uint64 * max(1, n))(*[int(b) for b, _ in rules])
+        en = (C.c_int32 * max(1, n))(*[ENGINES[e] for _, e in rules])
+        check(lib.mp_ctx_set_size_policy(self._ctx, mx, en, n))
+        self.size_policy = list(rules)
+
     def options(self) -> dict:
         o = _lib.mp_engine_opts()
         check(lib.mp_ctx_get_engine(self._ctx, C.byref(o)))

@@ -136,6 +136,43 @@ def tune(engine, sizes: list[int], grid: list[GridPoint] | None = None,
     return TuningTable(engine.topology.name, entries)
 
 
+def tune_engines(engine, sizes: list[int], reps: int = 10,
+                 mode: str = GRAPH_MODE) -> tuple[list[tuple[int, str]], list[dict]]:
+    """Measure the direct path by the SM transfer kernel and by a copy-engine
+    copy at every size; return the per-size policy for
+    `Engine.set_size_policy` (boundaries at the geometric mid-points between
+    tuned sizes) and the raw trials."""
+    import torch
+    sizes = sorted(sizes)
+    dev = engine.device_map[0]
+    big = torch.empty(sizes[-1], dtype=torch.uint8, device=f"cuda:{dev}")
+    out = torch.empty_like(big)
+    stream = torch.cuda.Stream(device=dev)
+    cfg = PathConfig(max_chunks=1, graph_mode=mode == GRAPH_MODE)
+    saved = engine.options()
+    engine.set_size_policy([])
+    trials = []
+    for eng_name in ("sm", "ce"):
+        engine.configure(direct=eng_name)
+        for s in sizes:
+            t = measure_makespan(engine, cfg, s, big[:s], out[:s], stream, reps)
+            trials.append({"bytes": s, "engine": eng_name, "seconds": t})
+    engine.configure(direct="sm" if saved["direct_engine"] == 0 else "ce")
+    best = {}
+    for s in sizes:
+        ts = {t["engine"]: t["seconds"] for t in trials if t["bytes"] == s}
+        best[s] = "sm" if ts["sm"] <= ts["ce"] else "ce"
+    rules: list[tuple[int, str]] = []
+    for i, s in enumerate(sizes):
+        bound = int(math.sqrt(s * sizes[i + 1])) if i + 1 < len(sizes) else 2**63 - 1
+        if rules and rules[-1][1] == best[s]:
+            rules[-1] = (bound, best[s])
+        else:
+            rules.append((bound, best[s]))
+    engine.clear_cache()
+    return rules, trials
+
+
 def calibrate_host_bandwidth(engine, link_bw: float, size: int, max_chunks: int,
                              candidates: list[float] | None = None, reps: int = 10,
                              name: str = "calibrated") -> tuple[float, Topology, list]:
