@@ -286,6 +286,26 @@ int mp_ctx_peer_matrix(const mp_ctx* ctx, int32_t* out, int32_t cap);
  * simulate_graph chain (sim.py:272-277). */
 int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size,
             int32_t src_dev, int32_t dst_dev, const mp_config* cfg, void* stream);
+/* One executed chunk-hop of a traced send (the GPU counterpart of the
+ * reference's SimTask, sim.py:32-49): first tile start / last tile
+ * completion (%globaltimer, SM lanes) or CE timing events, in microseconds
+ * from the send's fork on that device. */
+typedef struct {
+  int32_t node;              /* logical node id, build_graph order      */
+  int32_t engine;            /* MP_ENGINE_SM / MP_ENGINE_CE             */
+  int32_t device;            /* physical device index in the context    */
+  int32_t pad;
+  double start_us;
+  double end_us;
+} mp_trace_rec;
+
+/* Synchronous traced send (streamed program): writes one record per logical
+ * node (cap >= nodes; *n_out = nodes) — the real Timeline the reference's
+ * check_timeline (integrity.py:63-101) verifies. */
+int mp_send_trace(mp_ctx* ctx, const void* src, void* dst, uint64_t size,
+                  int32_t src_dev, int32_t dst_dev, const mp_config* cfg,
+                  mp_trace_rec* out, int32_t cap, int32_t* n_out);
+
 /* Receiver side: make `stream` (any device) wait for the last mp_send. */
 int mp_wait(mp_ctx* ctx, void* stream);
 int mp_send_stats_get(const mp_ctx* ctx, mp_send_stats* out);

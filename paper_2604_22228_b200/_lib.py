@@ -94,6 +94,11 @@ class mp_send_stats(C.Structure):
                 ("cache_misses", C.c_uint64), ("cache_evictions", C.c_uint64)]
 
 
+class mp_trace_rec(C.Structure):
+    _fields_ = [("node", C.c_int32), ("engine", C.c_int32), ("device", C.c_int32),
+                ("pad", C.c_int32), ("start_us", C.c_double), ("end_us", C.c_double)]
+
+
 class mp_engine_opts(C.Structure):
     _fields_ = [("direct_engine", C.c_int32), ("relay_engine", C.c_int32),
                 ("copy_kind", C.c_int32), ("ctas_per_sm", C.c_int32), ("threads", C.c_int32),
@@ -151,6 +156,8 @@ SIGNATURES = {
     "mp_ctx_peer_matrix": (C.c_int, [_vp, P(_i32), _i32]),
     "mp_send": (C.c_int, [_vp, _vp, _vp, _u64, _i32, _i32, P(mp_config), _vp]),
     "mp_wait": (C.c_int, [_vp, _vp]),
+    "mp_send_trace": (C.c_int, [_vp, _vp, _vp, _u64, _i32, _i32, P(mp_config), P(mp_trace_rec),
+                                _i32, P(_i32)]),
     "mp_send_stats_get": (C.c_int, [_vp, P(mp_send_stats)]),
     "mp_last_plan": (C.c_int, [_vp, P(mp_path), _i32, P(_i32), P(mp_chunk), _i32, P(_i32)]),
     "mp_cache_clear": (C.c_int, [_vp]),

@@ -46,7 +46,8 @@ namespace {
       throw Error{MP_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e)};     \
   } while (0)
 
-using KernelFn = void (*)(const mpk::Tile*, unsigned, mpk::Ctl*, unsigned, unsigned, unsigned);
+using KernelFn = void (*)(const mpk::Tile*, unsigned, mpk::Ctl*, unsigned, unsigned, unsigned,
+                          unsigned long long*);
 
 KernelFn pick_kernel(const mp_engine_opts& o) {
   if (o.copy_kind == MP_COPY_TMA) return mpk::transfer_kernel<1, 8>;
@@ -65,12 +66,13 @@ size_t kernel_smem(const mp_engine_opts& o) {
 // `nstatic` > 0 only for tables without flag waits: static first tiles must
 // never be waited on by another CTA (residency of every CTA is not guaranteed).
 void launch_transfer(const mp_engine_opts& o, unsigned grid, cudaStream_t s, const mpk::Tile* tiles,
-                     unsigned ntiles, mpk::Ctl* ctl, unsigned nstatic) {
+                     unsigned ntiles, mpk::Ctl* ctl, unsigned nstatic,
+                     unsigned long long* trace = nullptr) {
   KernelFn fn = pick_kernel(o);
   size_t smem = kernel_smem(o);
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   fn<<<grid, o.threads, smem, s>>>(tiles, ntiles, ctl, (unsigned)o.tma_stages, (unsigned)o.tma_block,
-                                   nstatic);
+                                   nstatic, trace);
   CK(cudaGetLastError());
 }
 
@@ -117,6 +119,7 @@ struct CeOp {
   size_t len;
   int wait_ev;     // index into the op-event list to wait on, -1 none
   int record_ev;   // index into the op-event list to record, -1 none
+  uint32_t node;   // logical graph node (chunk-hop) id, for traces
 };
 
 struct Program {
@@ -370,20 +373,24 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
     return (int)e->ev_phys.size() - 1;
   };
 
+  uint32_t node = 0;  // logical graph node of the chunk's first hop (graph.py:97-117)
   for (int c = 0; c < nc; ++c) {
     const mp_chunk& ch = e->chunks[c];
     const mp_path& P = e->paths[ch.path_index];
     const int p = ch.path_index;
     const uint64_t round = (uint64_t)ch.seq;
+    const uint32_t n_a = node, n_b = node + 1;
+    node += (uint32_t)P.nhops;
     if (P.kind == MP_PATH_DIRECT) {
       if (direct_sm) {
         int exec = o.pull ? dp : sp;
         mpk::Tile proto{};
+        proto.node = n_a;
         uint64_t tile = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[exec].sms);
         append_tiles(tiles[exec], 2 * round, s0 + ch.offset, d0 + ch.offset, ch.length, tile, proto);
       } else {
         e->ce.push_back(CeOp{sp, lane_base[p], (uint8_t*)dst + ch.offset, (const uint8_t*)src + ch.offset,
-                             (size_t)ch.length, -1, -1});
+                             (size_t)ch.length, -1, -1, n_a});
       }
     } else if (P.kind == MP_PATH_GPU) {
       Logi& L = ctx->logi[P.stage];
@@ -395,24 +402,28 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
       if (relay_sm) {
         uint64_t t1 = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[sp].sms);
         uint64_t t2 = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[rp].sms);
-        uint32_t n1 = (uint32_t)ntiles_of((uint64_t)(uintptr_t)stage, ch.length, t1);
-        uint32_t n2 = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, t2);
+        uint32_t k1 = (uint32_t)ntiles_of((uint64_t)(uintptr_t)stage, ch.length, t1);
+        uint32_t k2 = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, t2);
         mpk::Tile h1{};
         h1.signal = L.flags + c;
+        h1.node = n_a;
         append_tiles(tiles[sp], 2 * round, s0 + ch.offset, (uint64_t)(uintptr_t)stage, ch.length, t1, h1);
         mpk::Tile h2{};
         h2.wait = L.flags + c;
         h2.pass = L.flags + L.flag_cap + c;
-        h2.wait_count = n1;
-        h2.pass_count = n2;
+        h2.wait_count = k1;
+        h2.pass_count = k2;
         h2.flags = mpk::TILE_SRC_MUTABLE;
+        h2.node = n_b;
         // hop2 of round r is queued after hop1 of round r+1 (overlap, no stall)
         append_tiles(tiles[rp], 2 * round + 3, (uint64_t)(uintptr_t)stage, d0 + ch.offset, ch.length,
                      t2, h2);
       } else {
         int ev = new_event(sp);
-        e->ce.push_back(CeOp{sp, lane_base[p], stage, (const uint8_t*)src + ch.offset, (size_t)ch.length, -1, ev});
-        e->ce.push_back(CeOp{rp, lane_base[p] + 1, (uint8_t*)dst + ch.offset, stage, (size_t)ch.length, ev, -1});
+        e->ce.push_back(CeOp{sp, lane_base[p], stage, (const uint8_t*)src + ch.offset, (size_t)ch.length,
+                             -1, ev, n_a});
+        e->ce.push_back(CeOp{rp, lane_base[p] + 1, (uint8_t*)dst + ch.offset, stage, (size_t)ch.length,
+                             ev, -1, n_b});
       }
     } else if (host_sm) {
       // host-staged by the SM kernels: hop1 tiles (src device) bulk-store into
@@ -426,17 +437,19 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
       stage_off[p] += ch.length;
       const uint64_t th = std::min<uint64_t>(auto_tile_bytes(ctx, path_bytes[p], ctx->phys[sp].sms),
                                              kHostTileBytes);
-      uint32_t n1 = (uint32_t)ntiles_of((uint64_t)(uintptr_t)slot, ch.length, th);
-      uint32_t n2 = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, th);
+      uint32_t k1 = (uint32_t)ntiles_of((uint64_t)(uintptr_t)slot, ch.length, th);
+      uint32_t k2 = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, th);
       mpk::Tile h1{};
       h1.signal = L.flags + c;
+      h1.node = n_a;
       append_tiles(tiles[sp], 2 * round, s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
       mpk::Tile h2{};
       h2.wait = L.flags + c;
       h2.pass = L.flags + L.flag_cap + c;
-      h2.wait_count = n1;
-      h2.pass_count = n2;
+      h2.wait_count = k1;
+      h2.pass_count = k2;
       h2.flags = mpk::TILE_SRC_MUTABLE;
+      h2.node = n_b;
       append_tiles(tiles[dp], 2 * round + 3, (uint64_t)(uintptr_t)slot, d0 + ch.offset, ch.length, th, h2);
     } else {  // host-staged: D2H into pinned staging, H2D out of it (copy engines)
       int seq = ch.seq;
@@ -451,13 +464,15 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
         stage_off[p] += ch.length;
       }
       int ev1 = new_event(sp);
-      e->ce.push_back(CeOp{sp, lane_base[p], slot, (const uint8_t*)src + ch.offset, (size_t)ch.length, war, ev1});
+      e->ce.push_back(CeOp{sp, lane_base[p], slot, (const uint8_t*)src + ch.offset, (size_t)ch.length, war,
+                           ev1, n_a});
       int ev2 = -1;
       if (host_slots < path_count[p]) {
         ev2 = new_event(dp);
         hop2_done_ev[c] = ev2;
       }
-      e->ce.push_back(CeOp{dp, lane_base[p] + 1, (uint8_t*)dst + ch.offset, slot, (size_t)ch.length, ev1, ev2});
+      e->ce.push_back(CeOp{dp, lane_base[p] + 1, (uint8_t*)dst + ch.offset, slot, (size_t)ch.length, ev1,
+                           ev2, n_b});
     }
   }
   // upload one tile table per physical device
@@ -487,7 +502,18 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
 }
 
 // Enqueue the entry's work after `origin`, then make `origin` wait for it.
-void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing) {
+// Trace-mode resources (mp_send_trace): per physical device a stamp array
+// {first start, last end} per logical node plus a %globaltimer base, and
+// timing events around every copy-engine op.
+struct Trace {
+  int nodes = 0;
+  std::vector<unsigned long long*> stamps;  // per phys, 2 * nodes
+  std::vector<unsigned long long*> base;    // per phys, 1
+  std::vector<cudaEvent_t> base_ev;         // per phys, timing event at the fork
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ce_ev;  // per CE op
+};
+
+void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr = nullptr) {
   Phys& S = ctx->phys[e->src_phys];
   for (auto& p : ctx->phys) p.next_event = 0;
   CK(cudaSetDevice(S.ordinal));
@@ -501,6 +527,16 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing) {
     CK(cudaStreamWaitEvent(s, fork, 0));
     used.push_back({ph, s});
   };
+  if (tr) {  // time base of every device: a timing event + a %globaltimer stamp
+    for (size_t ph = 0; ph < ctx->phys.size(); ++ph) {
+      Phys& P = ctx->phys[ph];
+      use((int)ph, P.kstream);
+      CK(cudaSetDevice(P.ordinal));
+      CK(cudaEventRecord(tr->base_ev[ph], P.kstream));
+      mpk::stamp_kernel<<<1, 1, 0, P.kstream>>>(tr->base[ph]);
+      CK(cudaGetLastError());
+    }
+  }
   // SM transfer kernels, one per physical device
   for (auto& pr : e->progs) {
     Phys& P = ctx->phys[pr.phys];
@@ -508,19 +544,23 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing) {
     CK(cudaSetDevice(P.ordinal));
     bool t = timing && pr.phys == e->src_phys;
     if (t) CK(cudaEventRecord(P.kt0, P.kstream));
-    launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic);
+    launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic,
+                    tr ? tr->stamps[pr.phys] : nullptr);
     if (t) CK(cudaEventRecord(P.kt1, P.kstream));
   }
   // copy-engine lanes
   std::vector<cudaEvent_t> evs(e->ev_phys.size());
   for (size_t i = 0; i < evs.size(); ++i) evs[i] = take_event(ctx->phys[e->ev_phys[i]]);
-  for (const CeOp& op : e->ce) {
+  for (size_t i = 0; i < e->ce.size(); ++i) {
+    const CeOp& op = e->ce[i];
     Phys& P = ctx->phys[op.phys];
     cudaStream_t s = lane_stream(P, op.lane);
     use(op.phys, s);
     CK(cudaSetDevice(P.ordinal));
     if (op.wait_ev >= 0) CK(cudaStreamWaitEvent(s, evs[op.wait_ev], 0));
+    if (tr) CK(cudaEventRecord(tr->ce_ev[i].first, s));
     CK(cudaMemcpyAsync(op.dst, op.src, op.len, cudaMemcpyDefault, s));
+    if (tr) CK(cudaEventRecord(tr->ce_ev[i].second, s));
     if (op.record_ev >= 0) CK(cudaEventRecord(evs[op.record_ev], s));
   }
   // join
@@ -573,7 +613,53 @@ std::string make_key(const void* src, void* dst, uint64_t size, int sd, int dd, 
   return std::string((const char*)&k, sizeof k);
 }
 
+// LRU lookup; a miss plans, lowers and (graph mode) captures + instantiates
+// the entry, then evicts the least recent one past cfg.cache_capacity
+// (graph.py:173-186).  Updates the lifecycle stats.
+Entry* lookup_entry(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int src_dev, int dst_dev,
+                    const mp_config& cfg, cudaStream_t user) {
+  double t_start = now_us();
+  std::string key = make_key(src, dst, size, src_dev, dst_dev, cfg);
+  mp_send_stats& st = ctx->stats;
+  auto it = ctx->index.find(key);
+  if (it != ctx->index.end()) {
+    ctx->lru.splice(ctx->lru.end(), ctx->lru, it->second);
+    st.hit = 1;
+    st.cache_hits++;
+    st.creation_us = st.construction_us = st.instantiation_us = st.plan_us = 0.0;
+    return *it->second;
+  }
+  validate_config(cfg);
+  Entry* e = build_entry(ctx, key, src, dst, size, src_dev, dst_dev, cfg);
+  st.plan_us = now_us() - t_start;
+  st.creation_us = st.construction_us = st.instantiation_us = 0.0;
+  if (cfg.graph_mode) {
+    try {
+      capture(ctx, e);
+      e->graph = true;
+    } catch (...) {
+      destroy_entry(ctx, e);
+      throw;
+    }
+  }
+  ctx->lru.push_back(e);
+  ctx->index[key] = std::prev(ctx->lru.end());
+  while ((int)ctx->lru.size() > cfg.cache_capacity) {  // graph.py:184-185
+    Entry* old = ctx->lru.front();
+    ctx->lru.pop_front();
+    ctx->index.erase(old->key);
+    CK(cudaSetDevice(ctx->phys[old->src_phys].ordinal));
+    CK(cudaStreamSynchronize(user));  // old graph may still be replaying
+    destroy_entry(ctx, old);
+    st.cache_evictions++;
+  }
+  st.hit = 0;
+  st.cache_misses++;
+  return e;
+}
+
 }  // namespace
+
 
 // ===========================================================================
 // C ABI
@@ -775,47 +861,9 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
   if (!src || !dst) return fail(MP_ERR_VALUE, "null buffer");
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
-  double t_start = now_us();
   cudaStream_t user = (cudaStream_t)stream;
-  std::string key = make_key(src, dst, size, src_dev, dst_dev, *cfg);
-  Entry* e = nullptr;
-  auto it = ctx->index.find(key);
+  Entry* e = lookup_entry(ctx, src, dst, size, src_dev, dst_dev, *cfg, user);
   mp_send_stats& st = ctx->stats;
-  if (it != ctx->index.end()) {
-    ctx->lru.splice(ctx->lru.end(), ctx->lru, it->second);
-    e = *it->second;
-    st.hit = 1;
-    st.cache_hits++;
-    st.creation_us = st.construction_us = st.instantiation_us = st.plan_us = 0.0;
-  } else {
-    validate_config(*cfg);
-    e = build_entry(ctx, key, src, dst, size, src_dev, dst_dev, *cfg);
-    double t_plan = now_us();
-    st.plan_us = t_plan - t_start;
-    st.creation_us = st.construction_us = st.instantiation_us = 0.0;
-    if (cfg->graph_mode) {
-      try {
-        capture(ctx, e);
-        e->graph = true;
-      } catch (...) {
-        destroy_entry(ctx, e);
-        throw;
-      }
-    }
-    ctx->lru.push_back(e);
-    ctx->index[key] = std::prev(ctx->lru.end());
-    while ((int)ctx->lru.size() > cfg->cache_capacity) {  // graph.py:184-185
-      Entry* old = ctx->lru.front();
-      ctx->lru.pop_front();
-      ctx->index.erase(old->key);
-      CK(cudaSetDevice(ctx->phys[old->src_phys].ordinal));
-      CK(cudaStreamSynchronize(user));  // old graph may still be replaying
-      destroy_entry(ctx, old);
-      st.cache_evictions++;
-    }
-    st.hit = 0;
-    st.cache_misses++;
-  }
   Phys& S = ctx->phys[e->src_phys];
   CK(cudaSetDevice(S.ordinal));
   // serialise with a send issued on another stream (shared counters/arenas)
@@ -837,6 +885,110 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
   st.nodes_logical = e->nodes_logical;
   st.nodes_physical = e->nodes_physical;
   st.kernels = (int)e->progs.size();
+  ctx->last_paths = e->paths;
+  ctx->last_chunks = e->chunks;
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_send_trace(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_dev,
+                  int32_t dst_dev, const mp_config* cfg, mp_trace_rec* out, int32_t cap,
+                  int32_t* n_out) {
+  GUARD_BEGIN
+  if (!ctx || !cfg || !n_out) return fail(MP_ERR_VALUE, "null argument");
+  if (!ctx->has_topo) return fail(MP_ERR_STATE, "context has no topology (mp_ctx_set_topology)");
+  if (src_dev < 0 || src_dev >= (int)ctx->logi.size() || dst_dev < 0 || dst_dev >= (int)ctx->logi.size())
+    return fail(MP_ERR_PLAN, "transfers run between accelerators");
+  if (size == 0) return fail(MP_ERR_CHUNK, "message size must be >= 1 byte, got 0");
+  if (!src || !dst) return fail(MP_ERR_VALUE, "null buffer");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g;
+  mp_config c = *cfg;
+  c.graph_mode = 0;  // traced sends run the streamed program
+  Phys& S0 = ctx->phys[ctx->logi[src_dev].phys];
+  Entry* e = lookup_entry(ctx, src, dst, size, src_dev, dst_dev, c, S0.capture);
+  *n_out = e->nodes_logical;
+  if (cap < e->nodes_logical || !out) return fail(MP_ERR_CAPACITY, "trace capacity too small");
+  Trace tr;
+  tr.nodes = e->nodes_logical;
+  const size_t np = ctx->phys.size();
+  tr.stamps.assign(np, nullptr);
+  tr.base.assign(np, nullptr);
+  tr.base_ev.assign(np, nullptr);
+  std::vector<unsigned long long> init(2 * (size_t)tr.nodes);
+  for (int i = 0; i < tr.nodes; ++i) {
+    init[2 * i] = ~0ull;
+    init[2 * i + 1] = 0ull;
+  }
+  auto cleanup = [&]() {
+    for (size_t ph = 0; ph < np; ++ph) {
+      cudaSetDevice(ctx->phys[ph].ordinal);
+      if (tr.stamps[ph]) cudaFree(tr.stamps[ph]);
+      if (tr.base[ph]) cudaFree(tr.base[ph]);
+      if (tr.base_ev[ph]) cudaEventDestroy(tr.base_ev[ph]);
+    }
+    for (auto& p : tr.ce_ev) {
+      if (p.first) cudaEventDestroy(p.first);
+      if (p.second) cudaEventDestroy(p.second);
+    }
+  };
+  try {
+    for (size_t ph = 0; ph < np; ++ph) {
+      CK(cudaSetDevice(ctx->phys[ph].ordinal));
+      CK(cudaMalloc(&tr.stamps[ph], init.size() * sizeof(unsigned long long)));
+      CK(cudaMemcpy(tr.stamps[ph], init.data(), init.size() * sizeof(unsigned long long),
+                    cudaMemcpyHostToDevice));
+      CK(cudaMalloc(&tr.base[ph], sizeof(unsigned long long)));
+      CK(cudaEventCreate(&tr.base_ev[ph]));
+    }
+    for (const CeOp& op : e->ce) {
+      CK(cudaSetDevice(ctx->phys[op.phys].ordinal));
+      cudaEvent_t a, b;
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      tr.ce_ev.push_back({a, b});
+    }
+    Phys& S = ctx->phys[e->src_phys];
+    CK(cudaSetDevice(S.ordinal));
+    if (ctx->have_last) CK(cudaStreamWaitEvent(S.capture, ctx->last_done, 0));
+    enqueue(ctx, e, S.capture, false, &tr);
+    CK(cudaEventRecord(ctx->last_done, S.capture));
+    ctx->have_last = true;
+    ctx->last_stream = (void*)S.capture;
+    CK(cudaStreamSynchronize(S.capture));
+    for (int i = 0; i < tr.nodes; ++i) out[i] = mp_trace_rec{i, -1, -1, 0, 0.0, 0.0};
+    for (size_t ph = 0; ph < np; ++ph) {
+      CK(cudaSetDevice(ctx->phys[ph].ordinal));
+      std::vector<unsigned long long> st(init.size());
+      unsigned long long base = 0;
+      CK(cudaMemcpy(st.data(), tr.stamps[ph], st.size() * sizeof(unsigned long long),
+                    cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(&base, tr.base[ph], sizeof base, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < tr.nodes; ++i)
+        if (st[2 * i] != ~0ull) {
+          out[i].engine = MP_ENGINE_SM;
+          out[i].device = (int32_t)ph;
+          out[i].start_us = ((double)st[2 * i] - (double)base) * 1e-3;
+          out[i].end_us = ((double)st[2 * i + 1] - (double)base) * 1e-3;
+        }
+    }
+    for (size_t i = 0; i < e->ce.size(); ++i) {
+      const CeOp& op = e->ce[i];
+      CK(cudaSetDevice(ctx->phys[op.phys].ordinal));
+      float a = 0.f, b = 0.f;
+      CK(cudaEventElapsedTime(&a, tr.base_ev[op.phys], tr.ce_ev[i].first));
+      CK(cudaEventElapsedTime(&b, tr.base_ev[op.phys], tr.ce_ev[i].second));
+      mp_trace_rec& r = out[op.node];
+      r.engine = MP_ENGINE_CE;
+      r.device = op.phys;
+      r.start_us = a * 1e3;
+      r.end_us = b * 1e3;
+    }
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
   ctx->last_paths = e->paths;
   ctx->last_chunks = e->chunks;
   return MP_OK;

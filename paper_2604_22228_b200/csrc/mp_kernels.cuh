@@ -30,7 +30,7 @@ struct __align__(16) Tile {
   uint32_t wait_count;   // hop1 tiles of the chunk
   uint32_t pass_count;   // hop2 tiles of the chunk
   uint32_t flags;        // TILE_* bits
-  uint32_t pad;
+  uint32_t node;        // logical graph node (chunk-hop) id, for traces
 };
 
 enum : uint32_t {
@@ -212,11 +212,21 @@ __device__ __forceinline__ void release_signal(uint32_t* sig) {
   red_release_sys_add(sig, 1u);
 }
 
+// Trace stamps (trace mode only): per logical node, the first tile start and
+// the last tile completion in %globaltimer ns (array pre-set to {max, 0}).
+__device__ __forceinline__ void trace_start(unsigned long long* tr, uint32_t node) {
+  if (tr) atomicMin(&tr[2 * node], (unsigned long long)globaltimer());
+}
+__device__ __forceinline__ void trace_end(unsigned long long* tr, uint32_t node) {
+  if (tr) atomicMax(&tr[2 * node + 1], (unsigned long long)globaltimer());
+}
+
 // Per-stage bookkeeping of the TMA block stream.
 struct BlockMeta {
   uint8_t* dst;
   uint32_t bytes;
-  uint32_t* signal;  // set on the last block of a hop1 tile
+  uint32_t node_end;  // node + 1 on a tile's last block (trace mode), else 0
+  uint32_t* signal;   // set on the last block of a hop1 tile
 };
 
 // The TMA engine: thread 0 streams 16-byte-aligned tile bodies through the
@@ -235,11 +245,13 @@ struct TmaEngine {
   unsigned ntiles;
   Ctl* ctl;
   unsigned next_claim;
+  unsigned long long* trace;
   // loader cursor
   const uint8_t* ls = nullptr;
   uint8_t* ld = nullptr;
   uint64_t lrem = 0;
   uint32_t* lsig = nullptr;
+  uint32_t lnode_end = 0;
   int blocked = -1;  // -1 none, 0 table exhausted, 1 misaligned tile, 2 flag wait
   Tile pending;
   uint64_t g_load = 0, g_store = 0;
@@ -253,6 +265,7 @@ struct TmaEngine {
     const uint64_t body = (t.len - head) & ~(uint64_t)15;
     const uint64_t tail_at = head + body;
     const uint64_t tail = t.len - tail_at;
+    trace_start(trace, t.node);
     if (head | tail) {  // < 16 + 16 bytes: issue every load before any store
       uint8_t hb[15], tb[15];
 #pragma unroll
@@ -268,6 +281,7 @@ struct TmaEngine {
       }
     }
     if (body == 0) {
+      trace_end(trace, t.node);  // stamped before the release: hop2 cannot precede it
       if (t.signal) release_signal(t.signal);
       return;
     }
@@ -276,6 +290,7 @@ struct TmaEngine {
     ld = dst + head;
     lrem = body;
     lsig = t.signal;
+    lnode_end = trace ? t.node + 1 : 0;
   }
 
   // Make the loader cursor non-empty; false when blocked.  Claims run two
@@ -318,7 +333,7 @@ struct TmaEngine {
     if (!fetch()) return false;
     const uint32_t n = (uint32_t)(lrem < r.block ? lrem : r.block);
     const uint32_t s = (uint32_t)(g_load % r.stages);
-    meta[s] = BlockMeta{ld, n, lrem == n ? lsig : nullptr};
+    meta[s] = BlockMeta{ld, n, lrem == n ? lnode_end : 0u, lrem == n ? lsig : nullptr};
     mbar_expect_tx(&r.bar[s], n);
     tma_load(r.buf + (size_t)s * r.block, ls, n, &r.bar[s]);
     ls += n;
@@ -340,10 +355,11 @@ struct TmaEngine {
         tma_store(meta[s].dst, r.buf + (size_t)s * r.block, meta[s].bytes);
         bulk_commit();
         const uint64_t b = g_store++;
-        if (meta[s].signal) {  // hop1 tile complete: its bytes land before the release
+        if (meta[s].signal || meta[s].node_end) {  // tile complete: its bytes land first
           bulk_wait_all();
           fence_proxy_async();
-          release_signal(meta[s].signal);
+          if (meta[s].node_end) trace_end(trace, meta[s].node_end - 1);
+          if (meta[s].signal) release_signal(meta[s].signal);
         }
         if (b > seg) {  // refill the stage of block b-1 once its store has read smem
           bulk_wait_read<1>();
@@ -365,11 +381,15 @@ struct TmaEngine {
   }
 };
 
+// Time base of a traced send: %globaltimer at the fork point of this device.
+__global__ void stamp_kernel(unsigned long long* out) { *out = globaltimer(); }
+
 template <int KIND, int UNROLL>
 __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ tiles,
                                                        unsigned ntiles, Ctl* ctl,
                                                        unsigned stages, unsigned block,
-                                                       unsigned nstatic) {
+                                                       unsigned nstatic,
+                                                       unsigned long long* trace) {
   // Tiles [0, nstatic) (a prefix with no flag waits, nstatic <= gridDim.x) are
   // taken by CTA blockIdx.x without a claim; the rest are claimed dynamically.
   __shared__ Tile s_tile;
@@ -379,7 +399,8 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
   extern __shared__ __align__(128) uint8_t s_ring[];
   if (KIND == 1) {
     // ---- TMA: thread 0 streams; the CTA helps only with misaligned tiles ----
-    TmaEngine eng{TmaRing{s_ring, s_bar, 0u, stages, block}, s_meta, tiles, ntiles, ctl, 0u};
+    TmaEngine eng{TmaRing{s_ring, s_bar, 0u, stages, block}, s_meta, tiles, ntiles, ctl, 0u,
+                  trace};
     eng.nstatic = nstatic;
     if (threadIdx.x == 0) {
       for (unsigned s = 0; s < stages; ++s) mbar_init(&s_bar[s], 1);
@@ -387,7 +408,10 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       eng.prime();
     }
     for (;;) {
-      if (threadIdx.x == 0) s_cmd = eng.run(&s_tile);
+      if (threadIdx.x == 0) {
+        s_cmd = eng.run(&s_tile);
+        if (s_cmd) trace_start(trace, s_tile.node);
+      }
       __syncthreads();
       if (s_cmd == 0) break;
       const Tile& t = s_tile;
@@ -396,7 +420,10 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       else
         copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
       __syncthreads();  // every thread's stores precede the release
-      if (threadIdx.x == 0 && t.signal) release_signal(t.signal);
+      if (threadIdx.x == 0) {
+        trace_end(trace, t.node);
+        if (t.signal) release_signal(t.signal);
+      }
     }
     if (threadIdx.x == 0) bulk_wait_all();
   } else {
@@ -412,6 +439,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
         s_claim[parity] = atomicAdd(&ctl->work, 1u) + nstatic;  // prefetch the next claim
         s_tile = tiles[w];
         if (s_tile.wait) wait_tile_flag(s_tile, ctl);
+        trace_start(trace, s_tile.node);
       }
       __syncthreads();
       const Tile& t = s_tile;
@@ -420,7 +448,10 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       else
         copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
       __syncthreads();  // every thread's stores precede the release below
-      if (threadIdx.x == 0 && t.signal) release_signal(t.signal);
+      if (threadIdx.x == 0) {
+        trace_end(trace, t.node);
+        if (t.signal) release_signal(t.signal);
+      }
       w = s_claim[parity];
       parity ^= 1u;
       __syncthreads();  // s_tile / s_claim reuse

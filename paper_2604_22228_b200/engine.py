@@ -224,6 +224,37 @@ class Engine:
                    for c in chunks[:nchunks.value])
         return ps, cs
 
+    def trace(self, src, dst, nbytes: int | None = None, config: PathConfig | None = None,
+              src_dev: int | None = None, dst_dev: int | None = None):
+        """Send once (streamed program, synchronous) and return (plan, Timeline):
+        the real per-chunk-hop start/end times in the reference's Timeline
+        schema, checkable with `integrity.check_timeline` (integrity.py:63-101)."""
+        from .graph import build_graph
+        from .pipeline import ChunkPlan
+        from .paths import PathSet
+        from .timeline import from_records
+        from .topology import device_from_abi
+        config = config or PathConfig.from_env()
+        if nbytes is None:
+            nbytes = src.numel() * src.element_size()
+        if src_dev is None:
+            src_dev = self.device_map.index(src.device.index)
+        if dst_dev is None:
+            cands = [i for i, d in enumerate(self.device_map)
+                     if d == dst.device.index and i != src_dev]
+            dst_dev = cands[0]
+        cfg = config.abi()
+        n = C.c_int32()
+        lib.mp_send_trace(self._ctx, src.data_ptr(), dst.data_ptr(), nbytes, src_dev, dst_dev,
+                          C.byref(cfg), None, 0, C.byref(n))
+        recs = (_lib.mp_trace_rec * max(1, n.value))()
+        check(lib.mp_send_trace(self._ctx, src.data_ptr(), dst.data_ptr(), nbytes, src_dev,
+                                dst_dev, C.byref(cfg), recs, n.value, C.byref(n)))
+        paths, chunks = self.last_plan()
+        plan = ChunkPlan(nbytes, chunks, PathSet(device_from_abi(src_dev),
+                                                 device_from_abi(dst_dev), paths))
+        return plan, from_records(build_graph(plan), recs[:n.value])
+
     def clear_cache(self) -> None:
         check(lib.mp_cache_clear(self._ctx))
 
