@@ -71,6 +71,7 @@ class Clocks:
     def __init__(self, index=0):
         self.index = index
         self.samples = []
+        self._ready = threading.Event()
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
@@ -92,6 +93,7 @@ class Clocks:
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 self.samples.append([str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), str(mx)]
                                     + ["Active" if r & b else "Not Active" for b in bits])
+                self._ready.set()
                 self._stop.wait(0.01)
             return
         except Exception:
@@ -105,10 +107,12 @@ class Clocks:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
+            self._ready.set()
             self._stop.wait(0.2)
 
     def __enter__(self):
         self._t.start()
+        self._ready.wait(10.0)  # first sample taken before the timed region starts
         return self
 
     def __exit__(self, *exc):

@@ -330,9 +330,34 @@ int mp_kernel_time_ms(const mp_ctx* ctx, double* ms);
 
 /* ---- CUDA IPC (multi-process mode) --------------------------------------- */
 #define MP_IPC_HANDLE_BYTES 64
-int mp_ipc_export(const void* dev_ptr, int32_t device, uint8_t* handle_out);
+/* Handle of the allocation holding dev_ptr, and dev_ptr's offset in it. */
+int mp_ipc_export(const void* dev_ptr, int32_t device, uint8_t* handle_out,
+                  uint64_t* offset_out);
 int mp_ipc_import(const uint8_t* handle, int32_t device, void** dev_ptr_out);
 int mp_ipc_close(void* dev_ptr, int32_t device);
+
+/* ---- multi-process group mode (one process per GPU) ------------------------
+ * The paper's UCX cuda_ipc setting: ranks exchange CUDA-IPC
+ * handles once (rendezvous, cached) and every transfer is issued collectively:
+ * the source rank pushes Direct and hop1 tiles into IPC-mapped peer memory,
+ * each relay rank runs its hop2 tiles, the destination rank waits until all
+ * bytes landed.  A device-side generation barrier orders consecutive
+ * transfers, so cached CUDA graphs replay without host synchronisation.
+ * The host-staged path is single-process only. */
+#define MP_GROUP_BLOB_BYTES 256
+int mp_group_create(int32_t nranks, int32_t rank, int32_t device, uint64_t stage_bytes,
+                    int32_t flag_cap, mp_ctx** out);
+int mp_group_export(const mp_ctx* ctx, uint8_t* blob);
+int mp_group_import(mp_ctx* ctx, int32_t rank, const uint8_t* blob);
+/* Map a peer buffer (handle from mp_ipc_export) into this process, cached. */
+int mp_group_open(mp_ctx* ctx, const uint8_t* handle, uint64_t offset, void** ptr);
+/* Collective: every rank calls it for every transfer, in the same order.
+ * src: the sender's buffer (NULL elsewhere); src_align = src address mod 16
+ * (all ranks); dst: the destination buffer as mapped in this process. */
+int mp_group_send(mp_ctx* ctx, const void* src, uint32_t src_align, void* dst, uint64_t size,
+                  int32_t src_rank, int32_t dst_rank, const mp_config* cfg, void* stream);
+/* Role of this rank in the last transfer: 1 sender, 2 relay, 3 receiver, 0 none. */
+int mp_group_role(const mp_ctx* ctx, int32_t* role);
 
 #ifdef __cplusplus
 }

@@ -164,10 +164,19 @@ SIGNATURES = {
     "mp_sync": (C.c_int, [_vp]),
     "mp_measure_paths": (C.c_int, [_vp, _i32, _i32, _u64, _i32, P(C.c_double), _i32]),
     "mp_kernel_time_ms": (C.c_int, [_vp, P(C.c_double)]),
-    "mp_ipc_export": (C.c_int, [_vp, _i32, P(C.c_uint8)]),
+    "mp_ipc_export": (C.c_int, [_vp, _i32, P(C.c_uint8), P(_u64)]),
     "mp_ipc_import": (C.c_int, [P(C.c_uint8), _i32, P(_vp)]),
     "mp_ipc_close": (C.c_int, [_vp, _i32]),
+    "mp_group_create": (C.c_int, [_i32, _i32, _i32, _u64, _i32, P(_vp)]),
+    "mp_group_export": (C.c_int, [_vp, P(C.c_uint8)]),
+    "mp_group_import": (C.c_int, [_vp, _i32, P(C.c_uint8)]),
+    "mp_group_open": (C.c_int, [_vp, P(C.c_uint8), _u64, P(_vp)]),
+    "mp_group_send": (C.c_int, [_vp, _vp, C.c_uint32, _vp, _u64, _i32, _i32, P(mp_config), _vp]),
+    "mp_group_role": (C.c_int, [_vp, P(_i32)]),
 }
+
+MP_GROUP_BLOB_BYTES = 256
+MP_IPC_HANDLE_BYTES = 64
 
 
 def _load() -> C.CDLL:

@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <functional>
 #include <cstring>
 #include <list>
 #include <map>
@@ -47,7 +48,7 @@ namespace {
   } while (0)
 
 using KernelFn = void (*)(const mpk::Tile*, unsigned, mpk::Ctl*, unsigned, unsigned, unsigned,
-                          unsigned long long*);
+                          unsigned long long*, mpk::GroupSync);
 
 KernelFn pick_kernel(const mp_engine_opts& o) {
   if (o.copy_kind == MP_COPY_TMA) return mpk::transfer_kernel<1, 8>;
@@ -67,12 +68,14 @@ size_t kernel_smem(const mp_engine_opts& o) {
 // never be waited on by another CTA (residency of every CTA is not guaranteed).
 void launch_transfer(const mp_engine_opts& o, unsigned grid, cudaStream_t s, const mpk::Tile* tiles,
                      unsigned ntiles, mpk::Ctl* ctl, unsigned nstatic,
-                     unsigned long long* trace = nullptr) {
+                     unsigned long long* trace = nullptr, const mpk::GroupSync* gsync = nullptr) {
   KernelFn fn = pick_kernel(o);
   size_t smem = kernel_smem(o);
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  mpk::GroupSync g{};
+  if (gsync) g = *gsync;
   fn<<<grid, o.threads, smem, s>>>(tiles, ntiles, ctl, (unsigned)o.tma_stages, (unsigned)o.tma_block,
-                                   nstatic, trace);
+                                   nstatic, trace, g);
   CK(cudaGetLastError());
 }
 
@@ -142,11 +145,33 @@ struct Entry {
   cudaGraphExec_t exec = nullptr;
   int nodes_physical = 0;
   bool graph = false;
+  int grole = 0;                  // group mode: 0 none, 1 sender, 2 relay, 3 receiver
+  unsigned long long expected = 0;  // group receiver: bytes that must land
+};
+
+// Multi-process ("group") mode: one process per GPU.  Each rank owns a
+// resource block — relay staging arena, relay flags, and a sync block
+// {gen u32, seq u32, done u64} — exported as CUDA-IPC handles and mapped by
+// every other rank (peer access over NVLink).
+struct GroupState {
+  int rank = -1, nranks = 0;
+  uint8_t* stage = nullptr;
+  size_t stage_cap = 0;
+  uint32_t* flags = nullptr;  // [flag_cap] chunk flags + [flag_cap] pass counters
+  int flag_cap = 0;
+  uint8_t* sync = nullptr;    // gen @0, seq @4, done @8
+  std::vector<uint8_t*> peer_stage, peer_sync;
+  std::vector<uint32_t*> peer_flags;
+  std::vector<size_t> peer_stage_cap;
+  std::map<std::string, void*> opened;  // IPC-opened peer buffers by handle
+  uint32_t* gen(int q) { return (uint32_t*)(q == rank ? sync : peer_sync[q]); }
+  unsigned long long* done(int q) { return (unsigned long long*)((q == rank ? sync : peer_sync[q]) + 8); }
 };
 
 }  // namespace
 
 struct mp_ctx {
+  GroupState* group = nullptr;  // non-null: multi-process group context
   std::vector<Phys> phys;
   std::vector<Logi> logi;
   std::vector<int> peer;  // n_phys x n_phys can-access matrix
@@ -513,7 +538,47 @@ struct Trace {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ce_ev;  // per CE op
 };
 
+mpk::GroupSync group_sync(mp_ctx* ctx) {
+  GroupState* G = ctx->group;
+  mpk::GroupSync g{};
+  g.n = G->nranks;
+  for (int q = 0; q < G->nranks; ++q) g.gen[q] = G->gen(q);
+  g.seq = (uint32_t*)(G->sync + 4);
+  g.self_gen = G->gen(G->rank);
+  return g;
+}
+
+// Group mode: this rank's single kernel for the transfer — its tiles (sender
+// / relay), the completion wait (receiver) or just the barrier (others).
+void enqueue_group(mp_ctx* ctx, Entry* e, cudaStream_t origin) {
+  Phys& P = ctx->phys[0];
+  P.next_event = 0;
+  CK(cudaSetDevice(P.ordinal));
+  cudaEvent_t fork = take_event(P);
+  CK(cudaEventRecord(fork, origin));
+  CK(cudaStreamWaitEvent(P.kstream, fork, 0));
+  mpk::GroupSync g = group_sync(ctx);
+  if (!e->progs.empty()) {
+    const Program& pr = e->progs[0];
+    launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic, nullptr, &g);
+  } else if (e->grole == 3) {
+    mpk::group_recv_kernel<<<1, 32, 0, P.kstream>>>(g, ctx->group->done(ctx->group->rank), e->expected,
+                                                    P.ctl);
+    CK(cudaGetLastError());
+  } else {
+    mpk::group_noop_kernel<<<1, 32, 0, P.kstream>>>(g, P.ctl);
+    CK(cudaGetLastError());
+  }
+  cudaEvent_t j = take_event(P);
+  CK(cudaEventRecord(j, P.kstream));
+  CK(cudaStreamWaitEvent(origin, j, 0));
+}
+
 void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr = nullptr) {
+  if (ctx->group) {
+    enqueue_group(ctx, e, origin);
+    return;
+  }
   Phys& S = ctx->phys[e->src_phys];
   for (auto& p : ctx->phys) p.next_event = 0;
   CK(cudaSetDevice(S.ordinal));
@@ -617,7 +682,8 @@ std::string make_key(const void* src, void* dst, uint64_t size, int sd, int dd, 
 // the entry, then evicts the least recent one past cfg.cache_capacity
 // (graph.py:173-186).  Updates the lifecycle stats.
 Entry* lookup_entry(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int src_dev, int dst_dev,
-                    const mp_config& cfg, cudaStream_t user) {
+                    const mp_config& cfg, cudaStream_t user,
+                    const std::function<Entry*(const std::string&)>& builder = nullptr) {
   double t_start = now_us();
   std::string key = make_key(src, dst, size, src_dev, dst_dev, cfg);
   mp_send_stats& st = ctx->stats;
@@ -630,7 +696,7 @@ Entry* lookup_entry(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int 
     return *it->second;
   }
   validate_config(cfg);
-  Entry* e = build_entry(ctx, key, src, dst, size, src_dev, dst_dev, cfg);
+  Entry* e = builder ? builder(key) : build_entry(ctx, key, src, dst, size, src_dev, dst_dev, cfg);
   st.plan_us = now_us() - t_start;
   st.creation_us = st.construction_us = st.instantiation_us = 0.0;
   if (cfg.graph_mode) {
@@ -656,6 +722,127 @@ Entry* lookup_entry(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int 
   st.hit = 0;
   st.cache_misses++;
   return e;
+}
+
+
+// Serialized CUDA-IPC handles of one rank's group resource block.
+struct GroupBlob {
+  uint64_t stage_cap;
+  int32_t flag_cap;
+  int32_t rank;
+  cudaIpcMemHandle_t stage, flags, sync;
+};
+static_assert(sizeof(GroupBlob) <= MP_GROUP_BLOB_BYTES, "group blob size");
+
+// Group mode: lower the plan to THIS rank's part (every rank computes the same
+// plan, node ids, staging offsets and tile cuts deterministically).
+Entry* build_group_entry(mp_ctx* ctx, const std::string& key, const void* src, uint32_t src_align,
+                         void* dst, uint64_t size, int sr, int dr, const mp_config& cfg) {
+  GroupState* G = ctx->group;
+  std::unique_ptr<Entry> e(new Entry());
+  e->key = key;
+  e->paths = plan_paths(ctx->topo, sr, dr, cfg);
+  for (const mp_path& p : e->paths)
+    if (p.kind == MP_PATH_HOST)
+      throw Error{MP_ERR_STATE, "the host-staged path needs a single-process context "
+                                "(group mode moves the NVLink paths)"};
+  e->chunks = make_chunk_plan(e->paths.data(), (int)e->paths.size(), (int64_t)size, cfg.max_chunks);
+  const int np = (int)e->paths.size(), nc = (int)e->chunks.size();
+  for (const mp_chunk& c : e->chunks) e->nodes_logical += e->paths[c.path_index].nhops;
+  e->src_phys = 0;
+  const int me = G->rank;
+  e->grole = me == sr ? 1 : me == dr ? 3 : 0;
+  for (const mp_path& p : e->paths)
+    if (p.kind == MP_PATH_GPU && p.stage == me) e->grole = 2;
+  e->expected = size;
+  if (nc > G->flag_cap) throw Error{MP_ERR_STATE, "group flag array too small for the chunk plan"};
+  std::vector<uint64_t> path_bytes(np, 0);
+  for (const mp_chunk& c : e->chunks) path_bytes[c.path_index] += c.length;
+  const int sms = ctx->phys[0].sms;
+  const uint64_t s0 = (uint64_t)(uintptr_t)src, d0 = (uint64_t)(uintptr_t)dst;
+  std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>> tiles;
+  std::vector<uint64_t> stage_off(np, 0);
+  uint32_t node = 0;
+  for (int c = 0; c < nc; ++c) {
+    const mp_chunk& ch = e->chunks[c];
+    const mp_path& P = e->paths[ch.path_index];
+    const int p = ch.path_index;
+    const uint64_t round = (uint64_t)ch.seq;
+    const uint32_t n_a = node, n_b = node + 1;
+    node += (uint32_t)P.nhops;
+    if (P.kind == MP_PATH_DIRECT) {
+      if (e->grole != 1) continue;
+      mpk::Tile t{};
+      t.node = n_a;
+      t.signal = (uint32_t*)G->done(dr);  // bytes landed at the receiver
+      t.flags = mpk::TILE_SIGNAL_BYTES;
+      append_tiles(tiles, 2 * round, s0 + ch.offset, d0 + ch.offset, ch.length,
+                   auto_tile_bytes(ctx, path_bytes[p], sms), t);
+      continue;
+    }
+    const int k = P.stage;
+    stage_off[p] += (((uint64_t)src_align + ch.offset) - stage_off[p]) & 15u;
+    const uint64_t so = stage_off[p];
+    stage_off[p] += ch.length;
+    const size_t cap = k == me ? G->stage_cap : G->peer_stage_cap[k];
+    if (stage_off[p] > cap) throw Error{MP_ERR_STATE, "group staging arena too small for the relay share"};
+    const uint64_t t1 = auto_tile_bytes(ctx, path_bytes[p], sms);
+    if (e->grole == 1) {
+      uint8_t* stage = G->peer_stage[k] + so;
+      mpk::Tile h1{};
+      h1.node = n_a;
+      h1.signal = G->peer_flags[k] + c;
+      append_tiles(tiles, 2 * round, s0 + ch.offset, (uint64_t)(uintptr_t)stage, ch.length, t1, h1);
+    } else if (e->grole == 2 && k == me) {
+      uint8_t* stage = G->stage + so;
+      mpk::Tile h2{};
+      h2.node = n_b;
+      h2.wait = G->flags + c;
+      h2.pass = G->flags + G->flag_cap + c;
+      h2.wait_count = (uint32_t)ntiles_of((uint64_t)(uintptr_t)stage, ch.length, t1);
+      h2.pass_count = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, t1);
+      h2.signal = (uint32_t*)G->done(dr);
+      h2.flags = mpk::TILE_SRC_MUTABLE | mpk::TILE_SIGNAL_BYTES;
+      append_tiles(tiles, 2 * round + 3, (uint64_t)(uintptr_t)stage, d0 + ch.offset, ch.length, t1, h2);
+    }
+  }
+  if (!tiles.empty()) {
+    std::stable_sort(tiles.begin(), tiles.end(),
+                     [](const auto& a, const auto& b) { return a.first < b.first; });
+    std::vector<mpk::Tile> flat;
+    for (auto& kv : tiles) flat.push_back(kv.second);
+    Program pr;
+    pr.phys = 0;
+    pr.ntiles = (unsigned)flat.size();
+    pr.grid = (unsigned)std::min<uint64_t>(flat.size(), (uint64_t)sms * std::max(1, ctx->opts.ctas_per_sm));
+    bool waits = false;
+    for (const auto& t : flat) waits |= t.wait != nullptr;
+    pr.nstatic = waits ? 0u : pr.grid;
+    CK(cudaSetDevice(ctx->phys[0].ordinal));
+    CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile)));
+    CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
+    e->progs.push_back(pr);
+  }
+  return e.release();
+}
+
+// Base address of the allocation holding `p` (driver entry point, resolved at
+// run time so the library loads without libcuda on GPU-less hosts).
+uint64_t allocation_base(const void* p) {
+  using Fn = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static Fn fn = nullptr;
+  if (!fn) {
+    void* sym = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &sym, cudaEnableDefault, &q));
+    if (!sym) throw Error{MP_ERR_CUDA, "cuMemGetAddressRange unavailable"};
+    fn = (Fn)sym;
+  }
+  unsigned long long base = 0;
+  size_t sz = 0;
+  if (fn(&base, &sz, (unsigned long long)(uintptr_t)p) != 0)
+    throw Error{MP_ERR_CUDA, "cuMemGetAddressRange failed"};
+  return base;
 }
 
 }  // namespace
@@ -756,7 +943,23 @@ int mp_ctx_create(int32_t n_logical, const int32_t* device_map, mp_ctx** out) {
 void mp_ctx_destroy(mp_ctx* ctx) {
   if (!ctx) return;
   clear_cache(ctx);
+  if (GroupState* G = ctx->group) {
+    cudaSetDevice(ctx->phys[0].ordinal);
+    for (auto& kv : G->opened) cudaIpcCloseMemHandle(kv.second);
+    for (int q = 0; q < G->nranks; ++q) {
+      if (q == G->rank) continue;
+      if (G->peer_stage[q]) cudaIpcCloseMemHandle(G->peer_stage[q]);
+      if (G->peer_flags[q]) cudaIpcCloseMemHandle(G->peer_flags[q]);
+      if (G->peer_sync[q]) cudaIpcCloseMemHandle(G->peer_sync[q]);
+    }
+    cudaFree(G->stage);
+    cudaFree(G->flags);
+    cudaFree(G->sync);
+    delete G;
+    ctx->group = nullptr;
+  }
   for (auto& L : ctx->logi) {
+    if (L.phys < 0) continue;
     cudaSetDevice(ctx->phys[L.phys].ordinal);
     if (L.stage) cudaFree(L.stage);
     if (L.flags) cudaFree(L.flags);
@@ -852,6 +1055,7 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
   GUARD_BEGIN
   if (!ctx || !cfg) return fail(MP_ERR_VALUE, "null argument");
   if (!ctx->has_topo) return fail(MP_ERR_STATE, "context has no topology (mp_ctx_set_topology)");
+  if (ctx->group) return fail(MP_ERR_STATE, "group context: use mp_group_send");
   if (src_dev < 0 || src_dev >= (int)ctx->logi.size() || dst_dev < 0 || dst_dev >= (int)ctx->logi.size()) {
     if (src_dev == dst_dev)
       return fail(MP_ERR_PLAN, "source and destination are the same device (" + device_label(src_dev) + ")");
@@ -897,6 +1101,7 @@ int mp_send_trace(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_
   GUARD_BEGIN
   if (!ctx || !cfg || !n_out) return fail(MP_ERR_VALUE, "null argument");
   if (!ctx->has_topo) return fail(MP_ERR_STATE, "context has no topology (mp_ctx_set_topology)");
+  if (ctx->group) return fail(MP_ERR_STATE, "group context: use mp_group_send");
   if (src_dev < 0 || src_dev >= (int)ctx->logi.size() || dst_dev < 0 || dst_dev >= (int)ctx->logi.size())
     return fail(MP_ERR_PLAN, "transfers run between accelerators");
   if (size == 0) return fail(MP_ERR_CHUNK, "message size must be >= 1 byte, got 0");
@@ -1170,7 +1375,7 @@ int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t byt
   GUARD_END
 }
 
-int mp_ipc_export(const void* dev_ptr, int32_t device, uint8_t* handle_out) {
+int mp_ipc_export(const void* dev_ptr, int32_t device, uint8_t* handle_out, uint64_t* offset_out) {
   GUARD_BEGIN
   if (!dev_ptr || !handle_out) return fail(MP_ERR_VALUE, "null argument");
   DeviceGuard g;
@@ -1179,6 +1384,7 @@ int mp_ipc_export(const void* dev_ptr, int32_t device, uint8_t* handle_out) {
   CK(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
   static_assert(sizeof(h) == MP_IPC_HANDLE_BYTES, "ipc handle size");
   memcpy(handle_out, &h, sizeof h);
+  if (offset_out) *offset_out = (uint64_t)(uintptr_t)dev_ptr - allocation_base(dev_ptr);
   return MP_OK;
   GUARD_END
 }
@@ -1202,6 +1408,165 @@ int mp_ipc_close(void* dev_ptr, int32_t device) {
   CK(cudaIpcCloseMemHandle(dev_ptr));
   return MP_OK;
   GUARD_END
+}
+
+int mp_group_create(int32_t nranks, int32_t rank, int32_t device, uint64_t stage_bytes,
+                    int32_t flag_cap, mp_ctx** out) {
+  GUARD_BEGIN
+  if (!out || nranks < 1 || nranks > mpk::kMaxRanks || rank < 0 || rank >= nranks || flag_cap < 1)
+    return fail(MP_ERR_VALUE, "bad group arguments (1 <= nranks <= 16, 0 <= rank < nranks)");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(MP_ERR_VALUE, "device is not a CUDA device");
+  DeviceGuard g;
+  std::vector<int32_t> map(1, device);
+  mp_ctx* ctx = nullptr;
+  int rc = mp_ctx_create(1, map.data(), &ctx);
+  if (rc) return rc;
+  Logi local = ctx->logi[0];
+  ctx->logi.assign(nranks, Logi{});
+  for (auto& L : ctx->logi) L.phys = -1;
+  ctx->logi[rank] = local;
+  auto* G = new GroupState();
+  ctx->group = G;
+  G->rank = rank;
+  G->nranks = nranks;
+  G->flag_cap = flag_cap;
+  G->stage_cap = stage_bytes ? stage_bytes : 1;
+  G->peer_stage.assign(nranks, nullptr);
+  G->peer_sync.assign(nranks, nullptr);
+  G->peer_flags.assign(nranks, nullptr);
+  G->peer_stage_cap.assign(nranks, 0);
+  try {
+    CK(cudaSetDevice(device));
+    CK(cudaMalloc(&G->stage, G->stage_cap));
+    CK(cudaMalloc(&G->flags, (size_t)flag_cap * 2 * sizeof(uint32_t)));
+    CK(cudaMemset(G->flags, 0, (size_t)flag_cap * 2 * sizeof(uint32_t)));
+    CK(cudaMalloc(&G->sync, 256));
+    CK(cudaMemset(G->sync, 0, 256));
+    CK(cudaDeviceSynchronize());
+  } catch (...) {
+    mp_ctx_destroy(ctx);
+    throw;
+  }
+  *out = ctx;
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_group_export(const mp_ctx* ctx, uint8_t* blob) {
+  GUARD_BEGIN
+  if (!ctx || !ctx->group || !blob) return fail(MP_ERR_VALUE, "not a group context");
+  const GroupState* G = ctx->group;
+  DeviceGuard g;
+  CK(cudaSetDevice(ctx->phys[0].ordinal));
+  GroupBlob b{};
+  b.stage_cap = G->stage_cap;
+  b.flag_cap = G->flag_cap;
+  b.rank = G->rank;
+  CK(cudaIpcGetMemHandle(&b.stage, G->stage));
+  CK(cudaIpcGetMemHandle(&b.flags, G->flags));
+  CK(cudaIpcGetMemHandle(&b.sync, G->sync));
+  memset(blob, 0, MP_GROUP_BLOB_BYTES);
+  memcpy(blob, &b, sizeof b);
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_group_import(mp_ctx* ctx, int32_t rank, const uint8_t* blob) {
+  GUARD_BEGIN
+  if (!ctx || !ctx->group || !blob) return fail(MP_ERR_VALUE, "not a group context");
+  GroupState* G = ctx->group;
+  if (rank < 0 || rank >= G->nranks) return fail(MP_ERR_VALUE, "rank out of range");
+  if (rank == G->rank) return MP_OK;
+  GroupBlob b;
+  memcpy(&b, blob, sizeof b);
+  if (b.rank != rank) return fail(MP_ERR_VALUE, "blob belongs to another rank");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g;
+  CK(cudaSetDevice(ctx->phys[0].ordinal));
+  clear_cache(ctx);
+  void* p = nullptr;
+  CK(cudaIpcOpenMemHandle(&p, b.stage, cudaIpcMemLazyEnablePeerAccess));
+  G->peer_stage[rank] = (uint8_t*)p;
+  CK(cudaIpcOpenMemHandle(&p, b.flags, cudaIpcMemLazyEnablePeerAccess));
+  G->peer_flags[rank] = (uint32_t*)p;
+  CK(cudaIpcOpenMemHandle(&p, b.sync, cudaIpcMemLazyEnablePeerAccess));
+  G->peer_sync[rank] = (uint8_t*)p;
+  G->peer_stage_cap[rank] = b.stage_cap;
+  G->flag_cap = std::min(G->flag_cap, (int)b.flag_cap);
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_group_open(mp_ctx* ctx, const uint8_t* handle, uint64_t offset, void** ptr) {
+  GUARD_BEGIN
+  if (!ctx || !ctx->group || !handle || !ptr) return fail(MP_ERR_VALUE, "not a group context");
+  GroupState* G = ctx->group;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  std::string k((const char*)handle, MP_IPC_HANDLE_BYTES);
+  auto it = G->opened.find(k);
+  if (it == G->opened.end()) {
+    DeviceGuard g;
+    CK(cudaSetDevice(ctx->phys[0].ordinal));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof h);
+    void* base = nullptr;
+    CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    it = G->opened.emplace(k, base).first;
+  }
+  *ptr = (uint8_t*)it->second + offset;
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_group_send(mp_ctx* ctx, const void* src, uint32_t src_align, void* dst, uint64_t size,
+                  int32_t src_rank, int32_t dst_rank, const mp_config* cfg, void* stream) {
+  GUARD_BEGIN
+  if (!ctx || !ctx->group || !cfg) return fail(MP_ERR_VALUE, "not a group context");
+  GroupState* G = ctx->group;
+  if (!ctx->has_topo) return fail(MP_ERR_STATE, "context has no topology (mp_ctx_set_topology)");
+  if (src_rank < 0 || src_rank >= G->nranks || dst_rank < 0 || dst_rank >= G->nranks)
+    return fail(MP_ERR_PLAN, "transfers run between accelerators");
+  if (size == 0) return fail(MP_ERR_CHUNK, "message size must be >= 1 byte, got 0");
+  if (G->rank == src_rank && !src) return fail(MP_ERR_VALUE, "the sender needs its source buffer");
+  for (int q = 0; q < G->nranks; ++q)
+    if (q != G->rank && !G->peer_sync[q]) return fail(MP_ERR_STATE, "group peers not imported");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g;
+  cudaStream_t user = (cudaStream_t)stream;
+  const void* ksrc = G->rank == src_rank ? src : nullptr;
+  Entry* e = lookup_entry(ctx, ksrc, dst, size ^ ((uint64_t)src_align << 58), src_rank, dst_rank, *cfg,
+                          user, [&](const std::string& key) {
+                            return build_group_entry(ctx, key, ksrc, src_align & 15u, dst, size,
+                                                     src_rank, dst_rank, *cfg);
+                          });
+  mp_send_stats& st = ctx->stats;
+  CK(cudaSetDevice(ctx->phys[0].ordinal));
+  if (ctx->have_last && ctx->last_stream != stream) CK(cudaStreamWaitEvent(user, ctx->last_done, 0));
+  double t0 = now_us();
+  if (cfg->graph_mode && e->graph) CK(cudaGraphLaunch(e->exec, user));
+  else enqueue(ctx, e, user, false);
+  CK(cudaEventRecord(ctx->last_done, user));
+  ctx->have_last = true;
+  ctx->last_stream = stream;
+  st.launch_us = now_us() - t0;
+  st.graph_mode = cfg->graph_mode ? 1 : 0;
+  st.nodes_logical = e->nodes_logical;
+  st.nodes_physical = e->nodes_physical;
+  st.kernels = 1;
+  st.ce_copies = 0;
+  ctx->last_paths = e->paths;
+  ctx->last_chunks = e->chunks;
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_group_role(const mp_ctx* ctx, int32_t* role) {
+  if (!ctx || !ctx->group || !role) return fail(MP_ERR_VALUE, "not a group context");
+  std::lock_guard<std::mutex> lk(const_cast<mp_ctx*>(ctx)->mu);
+  *role = ctx->lru.empty() ? -1 : ctx->lru.back()->grole;
+  return MP_OK;
 }
 
 }  // extern "C"

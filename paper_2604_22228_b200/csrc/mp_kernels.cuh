@@ -35,6 +35,19 @@ struct __align__(16) Tile {
 
 enum : uint32_t {
   TILE_SRC_MUTABLE = 1u,  // source written during this launch (staging): no .nc loads
+  TILE_SIGNAL_BYTES = 2u, // signal is a u64 byte counter (+len), not a u32 tile count (+1)
+};
+
+// Cross-process ordering of consecutive group transfers (multi-process mode):
+// every rank's kernel for transfer n starts once every rank finished n-1
+// (gen[q] >= *seq), and its last CTA bumps *seq and its own gen.  All state is
+// in device memory, so a captured graph replays it unchanged.  n == 0: off.
+constexpr int kMaxRanks = 16;
+struct GroupSync {
+  uint32_t* gen[kMaxRanks];  // every rank's generation counter (IPC-mapped)
+  uint32_t* seq;             // this rank's transfer sequence number (local)
+  uint32_t* self_gen;        // this rank's generation counter (local)
+  int n;
 };
 
 struct __align__(16) Ctl {
@@ -212,6 +225,41 @@ __device__ __forceinline__ void release_signal(uint32_t* sig) {
   red_release_sys_add(sig, 1u);
 }
 
+// Completion signal of a tile: +1 on a u32 flag, or +bytes on a u64 counter.
+__device__ __forceinline__ void signal_tile(uint32_t* sig, uint64_t bytes) {
+  if (!bytes) {
+    release_signal(sig);
+    return;
+  }
+  __threadfence_system();
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(sig), "l"(bytes) : "memory");
+}
+
+__device__ __forceinline__ uint64_t sig_bytes(const Tile& t) {
+  return (t.flags & TILE_SIGNAL_BYTES) ? t.len : 0ull;
+}
+
+// Group barrier prologue (thread 0 of every CTA) with the 4 s safety timeout.
+__device__ __forceinline__ void group_wait(const GroupSync& g, Ctl* ctl) {
+  if (g.n == 0) return;
+  const uint32_t want = *(volatile uint32_t*)g.seq;
+  const uint64_t t0 = globaltimer();
+  for (int q = 0; q < g.n; ++q)
+    while (ld_acquire_sys(g.gen[q]) < want) {
+      if (globaltimer() - t0 > kWaitTimeoutNs) {
+        atomicExch(&ctl->error, 2u);
+        return;
+      }
+      __nanosleep(128);
+    }
+}
+
+__device__ __forceinline__ void group_done(const GroupSync& g) {
+  if (g.n == 0) return;
+  *(volatile uint32_t*)g.seq = *(volatile uint32_t*)g.seq + 1u;
+  release_signal(g.self_gen);
+}
+
 // Trace stamps (trace mode only): per logical node, the first tile start and
 // the last tile completion in %globaltimer ns (array pre-set to {max, 0}).
 __device__ __forceinline__ void trace_start(unsigned long long* tr, uint32_t node) {
@@ -226,7 +274,8 @@ struct BlockMeta {
   uint8_t* dst;
   uint32_t bytes;
   uint32_t node_end;  // node + 1 on a tile's last block (trace mode), else 0
-  uint32_t* signal;   // set on the last block of a hop1 tile
+  uint32_t* signal;   // set on a tile's last block when the tile signals
+  uint64_t sig_bytes; // 0: +1 on a u32 flag; else +bytes on a u64 counter
 };
 
 // The TMA engine: thread 0 streams 16-byte-aligned tile bodies through the
@@ -251,6 +300,7 @@ struct TmaEngine {
   uint8_t* ld = nullptr;
   uint64_t lrem = 0;
   uint32_t* lsig = nullptr;
+  uint64_t lsig_bytes = 0;
   uint32_t lnode_end = 0;
   int blocked = -1;  // -1 none, 0 table exhausted, 1 misaligned tile, 2 flag wait
   Tile pending;
@@ -282,7 +332,7 @@ struct TmaEngine {
     }
     if (body == 0) {
       trace_end(trace, t.node);  // stamped before the release: hop2 cannot precede it
-      if (t.signal) release_signal(t.signal);
+      if (t.signal) signal_tile(t.signal, sig_bytes(t));
       return;
     }
     if (mut) fence_proxy_async();  // staged bytes were written by the generic proxy
@@ -290,6 +340,7 @@ struct TmaEngine {
     ld = dst + head;
     lrem = body;
     lsig = t.signal;
+    lsig_bytes = sig_bytes(t);
     lnode_end = trace ? t.node + 1 : 0;
   }
 
@@ -333,7 +384,7 @@ struct TmaEngine {
     if (!fetch()) return false;
     const uint32_t n = (uint32_t)(lrem < r.block ? lrem : r.block);
     const uint32_t s = (uint32_t)(g_load % r.stages);
-    meta[s] = BlockMeta{ld, n, lrem == n ? lnode_end : 0u, lrem == n ? lsig : nullptr};
+    meta[s] = BlockMeta{ld, n, lrem == n ? lnode_end : 0u, lrem == n ? lsig : nullptr, lsig_bytes};
     mbar_expect_tx(&r.bar[s], n);
     tma_load(r.buf + (size_t)s * r.block, ls, n, &r.bar[s]);
     ls += n;
@@ -359,7 +410,7 @@ struct TmaEngine {
           bulk_wait_all();
           fence_proxy_async();
           if (meta[s].node_end) trace_end(trace, meta[s].node_end - 1);
-          if (meta[s].signal) release_signal(meta[s].signal);
+          if (meta[s].signal) signal_tile(meta[s].signal, meta[s].sig_bytes);
         }
         if (b > seg) {  // refill the stage of block b-1 once its store has read smem
           bulk_wait_read<1>();
@@ -389,7 +440,8 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
                                                        unsigned ntiles, Ctl* ctl,
                                                        unsigned stages, unsigned block,
                                                        unsigned nstatic,
-                                                       unsigned long long* trace) {
+                                                       unsigned long long* trace,
+                                                       GroupSync gsync) {
   // Tiles [0, nstatic) (a prefix with no flag waits, nstatic <= gridDim.x) are
   // taken by CTA blockIdx.x without a claim; the rest are claimed dynamically.
   __shared__ Tile s_tile;
@@ -397,6 +449,8 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
   __shared__ uint64_t s_bar[16];
   __shared__ BlockMeta s_meta[16];
   extern __shared__ __align__(128) uint8_t s_ring[];
+  if (threadIdx.x == 0) group_wait(gsync, ctl);
+  __syncthreads();
   if (KIND == 1) {
     // ---- TMA: thread 0 streams; the CTA helps only with misaligned tiles ----
     TmaEngine eng{TmaRing{s_ring, s_bar, 0u, stages, block}, s_meta, tiles, ntiles, ctl, 0u,
@@ -422,7 +476,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       __syncthreads();  // every thread's stores precede the release
       if (threadIdx.x == 0) {
         trace_end(trace, t.node);
-        if (t.signal) release_signal(t.signal);
+        if (t.signal) signal_tile(t.signal, sig_bytes(t));
       }
     }
     if (threadIdx.x == 0) bulk_wait_all();
@@ -450,7 +504,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       __syncthreads();  // every thread's stores precede the release below
       if (threadIdx.x == 0) {
         trace_end(trace, t.node);
-        if (t.signal) release_signal(t.signal);
+        if (t.signal) signal_tile(t.signal, sig_bytes(t));
       }
       w = s_claim[parity];
       parity ^= 1u;
@@ -464,8 +518,36 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       ctl->exit = 0u;
       ctl->launches += 1u;
       __threadfence();
+      group_done(gsync);
     }
   }
+}
+
+// Receiver side of a group transfer: wait until `expected` bytes have landed
+// (direct and hop2 tiles add their sizes to *done), re-arm, finish the barrier.
+__global__ void group_recv_kernel(GroupSync gsync, unsigned long long* done,
+                                  unsigned long long expected, Ctl* ctl) {
+  group_wait(gsync, ctl);
+  const uint64_t t0 = globaltimer();
+  while (true) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(done) : "memory");
+    if (v >= expected) break;
+    if (globaltimer() - t0 > kWaitTimeoutNs) {
+      atomicExch(&ctl->error, 3u);
+      break;
+    }
+    __nanosleep(128);
+  }
+  *(volatile unsigned long long*)done = 0ull;
+  __threadfence_system();
+  group_done(gsync);
+}
+
+// A rank with no part in a group transfer still takes part in its barrier.
+__global__ void group_noop_kernel(GroupSync gsync, Ctl* ctl) {
+  group_wait(gsync, ctl);
+  group_done(gsync);
 }
 
 }  // namespace mpk

@@ -1,0 +1,61 @@
+"""Multi-process group mode on one B200: 2-3 processes share cuda:0 through
+CUDA IPC (each rank is a logical GPU).  The receiver's bytes must equal the
+oracle's, over several back-to-back transfers (device barrier + flag re-arm),
+in streamed and cached-graph modes, direct-only and with a relay rank."""
+
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
+import _dist_util  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _worker(rank, world, port, gpu_paths, graph, size, reps):
+    import numpy as np
+    import torch.distributed as dist
+
+    import paper_2604_22228_b200 as mp
+    from oracle import transfer as ot
+    from paper_2604_22228_b200.group import TransferGroup
+    _dist_util.init(rank, world, port)
+    torch.cuda.set_device(0)
+    topo = mp.load_topology(mp.mesh_text("g", world, 7.5e11, 1, 2e-6, 5.5e10, 1e-5, "full"))
+    grp = TransferGroup(topo, device=0, stage_bytes=64 << 20)
+    src = torch.empty(size + 3, dtype=torch.uint8, device="cuda:0")[3:]  # unaligned on purpose
+    dst = torch.empty(size, dtype=torch.uint8, device="cuda:0")
+    sb = grp.expose(src, owner=0)
+    db = grp.expose(dst, owner=1)
+    cfg = mp.PathConfig(num_gpu_paths=gpu_paths, max_chunks=4, graph_mode=graph,
+                        share_policy="equal")
+    for r in range(reps):
+        data = ot.pattern(size, seed=100 + r)
+        if rank == 0:
+            src.copy_(torch.from_numpy(data))
+        if rank == 1:
+            dst.fill_(0xA5)
+        torch.cuda.synchronize()
+        dist.barrier()
+        grp.transfer(sb, db, size, cfg)
+        torch.cuda.synchronize()
+        grp.sync()
+        if rank == 1:
+            got = dst.cpu().numpy()
+            assert np.array_equal(got, data), f"rep {r}: mismatch"
+        dist.barrier()
+    assert grp.role() == {0: 1, 1: 3}.get(rank, 2 if rank < gpu_paths + 1 else 0)
+    grp.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,gpu_paths", [(2, 1), (3, 2), (4, 2)])
+@pytest.mark.parametrize("graph", [False, True])
+def test_group_transfer(world, gpu_paths, graph):
+    _dist_util.run(_worker, world, gpu_paths, graph, (4 << 20) + 12345, 3)
