@@ -286,6 +286,23 @@ int mp_ctx_peer_matrix(const mp_ctx* ctx, int32_t* out, int32_t cap);
  * simulate_graph chain (sim.py:272-277). */
 int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size,
             int32_t src_dev, int32_t dst_dev, const mp_config* cfg, void* stream);
+/* One transfer of a concurrent batch. */
+typedef struct {
+  const void* src;
+  void* dst;
+  uint64_t size;
+  int32_t src_dev, dst_dev;
+} mp_xfer;
+
+/* Concurrent transfers (windows, bidirectional flows, ring halo exchanges —
+ * the reference's simulate_concurrent, sim.py:287-292) as ONE program: the
+ * tiles of every transfer share one persistent kernel per device,
+ * interleaved round by round, and the whole batch is one cached graph.
+ * joint = 1 chooses staging devices with plan_contention_free
+ * (paths.py:210-242); 0 plans each transfer with plan_paths. */
+int mp_send_many(mp_ctx* ctx, const mp_xfer* xfers, int32_t n, const mp_config* cfg,
+                 int32_t joint, void* stream);
+
 /* One executed chunk-hop of a traced send (the GPU counterpart of the
  * reference's SimTask, sim.py:32-49): first tile start / last tile
  * completion (%globaltimer, SM lanes) or CE timing events, in microseconds

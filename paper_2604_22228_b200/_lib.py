@@ -99,6 +99,11 @@ class mp_trace_rec(C.Structure):
                 ("pad", C.c_int32), ("start_us", C.c_double), ("end_us", C.c_double)]
 
 
+class mp_xfer(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p), ("size", C.c_uint64),
+                ("src_dev", C.c_int32), ("dst_dev", C.c_int32)]
+
+
 class mp_engine_opts(C.Structure):
     _fields_ = [("direct_engine", C.c_int32), ("relay_engine", C.c_int32),
                 ("copy_kind", C.c_int32), ("ctas_per_sm", C.c_int32), ("threads", C.c_int32),
@@ -156,6 +161,7 @@ SIGNATURES = {
     "mp_ctx_peer_matrix": (C.c_int, [_vp, P(_i32), _i32]),
     "mp_send": (C.c_int, [_vp, _vp, _vp, _u64, _i32, _i32, P(mp_config), _vp]),
     "mp_wait": (C.c_int, [_vp, _vp]),
+    "mp_send_many": (C.c_int, [_vp, P(mp_xfer), _i32, P(mp_config), _i32, _vp]),
     "mp_send_trace": (C.c_int, [_vp, _vp, _vp, _u64, _i32, _i32, P(mp_config), P(mp_trace_rec),
                                 _i32, P(_i32)]),
     "mp_send_stats_get": (C.c_int, [_vp, P(mp_send_stats)]),

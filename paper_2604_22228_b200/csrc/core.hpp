@@ -50,6 +50,9 @@ std::string device_label(int dev);  // "3" or "host"
 // ---- planner ---------------------------------------------------------------
 double py_sum(const std::vector<double>& xs);  // CPython >= 3.12 sum() of floats
 std::vector<mp_path> plan_paths(const Topology& t, int src, int dst, const mp_config& cfg);
+std::vector<std::vector<mp_path>> plan_contention_free_sets(
+    const Topology& t, const std::vector<std::pair<int, int>>& transfers, const mp_config& cfg,
+    int* shared_out);
 void validate_config(const mp_config& cfg);
 void validate_pathset(const mp_path* paths, int n);
 std::vector<mp_chunk> make_chunk_plan(const mp_path* paths, int n, int64_t size,

@@ -642,7 +642,7 @@ static std::vector<int> pathset_channels(const std::vector<mp_path>& ps) {  // p
 }
 
 // paths.py:210-242 plan_contention_free
-static std::vector<std::vector<mp_path>> plan_contention_free(
+std::vector<std::vector<mp_path>> plan_contention_free_sets(
     const Topology& t, const std::vector<std::pair<int, int>>& transfers, const mp_config& cfg,
     int* shared_out) {
   validate_config(cfg);
@@ -940,7 +940,7 @@ int mp_plan_contention_free(const mp_topology* topo, const int32_t* srcs, const 
   std::vector<std::pair<int, int>> tr;
   for (int i = 0; i < n_transfers; ++i) tr.emplace_back(srcs[i], dsts[i]);
   int sh = 0;
-  auto sets = plan_contention_free(topo->t, tr, *cfg, &sh);
+  auto sets = plan_contention_free_sets(topo->t, tr, *cfg, &sh);
   std::vector<mp_path> flat;
   for (auto& s : sets) flat.insert(flat.end(), s.begin(), s.end());
   if (paths_per_set) *paths_per_set = sets.empty() ? 0 : (int32_t)sets[0].size();

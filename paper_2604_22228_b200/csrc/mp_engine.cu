@@ -327,181 +327,237 @@ uint64_t ntiles_of(uint64_t dst, uint64_t len, uint64_t tile) {
   return tile_cuts(dst, len, tile).size() - 1;
 }
 
-// Lower a chunk plan to device programs and copy-engine ops.
-Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* dst, uint64_t size,
-                   int src_dev, int dst_dev, const mp_config& cfg) {
-  auto* e = new Entry();
-  e->key = key;
-  e->paths = plan_paths(ctx->topo, src_dev, dst_dev, cfg);
-  e->chunks = make_chunk_plan(e->paths.data(), (int)e->paths.size(), (int64_t)size, cfg.max_chunks);
-  const int np = (int)e->paths.size();
-  const int nc = (int)e->chunks.size();
-  for (const mp_chunk& c : e->chunks) e->nodes_logical += e->paths[c.path_index].nhops;
-  const mp_engine_opts& o = ctx->opts;
-  const int sp = ctx->logi[src_dev].phys, dp = ctx->logi[dst_dev].phys;
-  e->src_phys = sp;
+// One transfer of a (possibly multi-transfer) program.
+struct Xfer {
+  const void* src;
+  void* dst;
+  uint64_t size;
+  int sd, dd;                  // logical source / destination
+  std::vector<mp_path> paths;  // pre-planned (joint planning) or empty
+};
 
-  // per-path byte totals and nominal lengths
-  std::vector<uint64_t> path_bytes(np, 0), nominal(np, 0);
-  std::vector<int> path_count(np, 0);
-  for (const mp_chunk& c : e->chunks) {
-    path_bytes[c.path_index] += c.length;
-    nominal[c.path_index] = std::max<uint64_t>(nominal[c.path_index], c.length);
-    path_count[c.path_index] += 1;
-  }
-  // engines per path type for this message size (measured thresholds)
-  const bool sm_ok = size >= (uint64_t)o.sm_min_bytes;
-  int direct_engine = o.direct_engine;
-  for (const auto& rule : ctx->size_policy)
-    if (size <= rule.first) {
-      direct_engine = rule.second;
-      break;
+// Lower one or more transfers to device programs and copy-engine ops: ONE
+// tile table (one kernel) per physical device for every NVLink/HBM chunk-hop
+// of every transfer, interleaved round by round so concurrent transfers
+// progress together; copy-engine lanes per (transfer, path, hop).
+Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> xs,
+                         const mp_config& cfg) {
+  struct Guard {  // frees device tables of a half-built entry on error
+    mp_ctx* ctx;
+    Entry* e;
+    ~Guard() {
+      if (e) destroy_entry(ctx, e);
     }
-  const bool direct_sm = direct_engine == MP_ENGINE_SM && sm_ok;
-  const bool relay_sm = o.relay_engine == MP_ENGINE_SM && sm_ok;
-  const bool host_sm = o.host_engine == MP_ENGINE_SM && sm_ok;
-  // staging requirements
+    Entry* operator->() { return e; }
+    Entry* release() {
+      Entry* r = e;
+      e = nullptr;
+      return r;
+    }
+  } e{ctx, new Entry()};
+  e->key = key;
+  const mp_engine_opts& o = ctx->opts;
+  const int T = (int)xs.size();
+  if (T < 1 || T > 64) throw Error{MP_ERR_VALUE, "1..64 transfers per program"};
+  std::vector<std::vector<mp_chunk>> chunks(T);
+  std::vector<int> chunk_base(T, 0);
+  int total_chunks = 0;
+  for (int t = 0; t < T; ++t) {
+    if (xs[t].paths.empty()) xs[t].paths = plan_paths(ctx->topo, xs[t].sd, xs[t].dd, cfg);
+    chunks[t] = make_chunk_plan(xs[t].paths.data(), (int)xs[t].paths.size(), (int64_t)xs[t].size,
+                                cfg.max_chunks);
+    chunk_base[t] = total_chunks;
+    total_chunks += (int)chunks[t].size();
+    for (const mp_chunk& c : chunks[t]) e->nodes_logical += xs[t].paths[c.path_index].nhops;
+  }
+  e->paths = xs[0].paths;
+  e->chunks = chunks[0];
+  e->src_phys = ctx->logi[xs[0].sd].phys;
+
+  struct PathInfo {
+    uint64_t bytes = 0, nominal = 0;
+    int count = 0;
+  };
+  struct Engines {
+    bool direct_sm, relay_sm, host_sm;
+    int host_slots;
+  };
+  std::vector<std::vector<PathInfo>> info(T);
+  std::vector<Engines> eng(T);
   std::vector<size_t> stage_need(ctx->logi.size(), 0);
   std::vector<char> flag_devs(ctx->logi.size(), 0);
   size_t host_need = 0;
-  int host_slots = 0;
-  for (int p = 0; p < np; ++p) {
-    if (e->paths[p].kind == MP_PATH_GPU) {
-      stage_need[e->paths[p].stage] = path_bytes[p] + 16 * (size_t)path_count[p];
-      if (relay_sm) flag_devs[e->paths[p].stage] = 1;
+  for (int t = 0; t < T; ++t) {
+    const auto& paths = xs[t].paths;
+    info[t].assign(paths.size(), PathInfo{});
+    for (const mp_chunk& c : chunks[t]) {
+      PathInfo& pi = info[t][c.path_index];
+      pi.bytes += c.length;
+      pi.nominal = std::max<uint64_t>(pi.nominal, c.length);
+      pi.count += 1;
     }
-    if (e->paths[p].kind == MP_PATH_HOST) {
-      // the SM host path keeps every chunk resident (its share is a few MB)
-      host_slots = (o.host_slots > 0 && !host_sm) ? std::min(o.host_slots, path_count[p]) : path_count[p];
-      host_need = host_slots < path_count[p] ? (size_t)host_slots * nominal[p]
-                                              : path_bytes[p] + 16 * (size_t)path_count[p];
-      if (host_sm) flag_devs[dst_dev] = 1;
+    // engines per path type for this message size (measured policy)
+    const bool sm_ok = xs[t].size >= (uint64_t)o.sm_min_bytes;
+    int direct_engine = o.direct_engine;
+    for (const auto& rule : ctx->size_policy)
+      if (xs[t].size <= rule.first) {
+        direct_engine = rule.second;
+        break;
+      }
+    eng[t] = Engines{direct_engine == MP_ENGINE_SM && sm_ok, o.relay_engine == MP_ENGINE_SM && sm_ok,
+                     o.host_engine == MP_ENGINE_SM && sm_ok, 0};
+    for (size_t p = 0; p < paths.size(); ++p) {
+      const PathInfo& pi = info[t][p];
+      if (paths[p].kind == MP_PATH_GPU) {
+        stage_need[paths[p].stage] += pi.bytes + 16 * (size_t)pi.count;
+        if (eng[t].relay_sm) flag_devs[paths[p].stage] = 1;
+      }
+      if (paths[p].kind == MP_PATH_HOST) {
+        // the SM host path keeps every chunk resident (its share is a few MB)
+        eng[t].host_slots = (o.host_slots > 0 && !eng[t].host_sm) ? std::min(o.host_slots, pi.count)
+                                                                   : pi.count;
+        host_need += eng[t].host_slots < pi.count ? (size_t)eng[t].host_slots * pi.nominal
+                                                  : pi.bytes + 16 * (size_t)pi.count;
+        if (eng[t].host_sm) flag_devs[xs[t].dd] = 1;
+      }
     }
   }
-  ensure_arenas(ctx, stage_need, flag_devs, nc, host_need);
+  ensure_arenas(ctx, stage_need, flag_devs, total_chunks, host_need);
 
-  const uint64_t s0 = (uint64_t)(uintptr_t)src, d0 = (uint64_t)(uintptr_t)dst;
   std::vector<std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>> tiles(ctx->phys.size());
-  std::vector<uint64_t> stage_off(np, 0);
-  std::vector<int> lane_base(np, 0);
-  {
-    int l = 0;
-    for (int p = 0; p < np; ++p) {
-      lane_base[p] = l;
-      l += e->paths[p].nhops;
-    }
-  }
-  std::vector<int> hop2_done_ev(nc, -1);  // host WAR: event recorded after hop2 of chunk
-  std::vector<int> host_chunk_of_seq;
+  std::vector<uint64_t> stage_cursor(ctx->logi.size(), 0);  // shared relay arenas
+  uint64_t host_cursor = 0;                                  // shared pinned arena
   auto new_event = [&](int phys) {
     e->ev_phys.push_back(phys);
     return (int)e->ev_phys.size() - 1;
   };
-
-  uint32_t node = 0;  // logical graph node of the chunk's first hop (graph.py:97-117)
-  for (int c = 0; c < nc; ++c) {
-    const mp_chunk& ch = e->chunks[c];
-    const mp_path& P = e->paths[ch.path_index];
-    const int p = ch.path_index;
-    const uint64_t round = (uint64_t)ch.seq;
-    const uint32_t n_a = node, n_b = node + 1;
-    node += (uint32_t)P.nhops;
-    if (P.kind == MP_PATH_DIRECT) {
-      if (direct_sm) {
-        int exec = o.pull ? dp : sp;
-        mpk::Tile proto{};
-        proto.node = n_a;
-        uint64_t tile = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[exec].sms);
-        append_tiles(tiles[exec], 2 * round, s0 + ch.offset, d0 + ch.offset, ch.length, tile, proto);
-      } else {
-        e->ce.push_back(CeOp{sp, lane_base[p], (uint8_t*)dst + ch.offset, (const uint8_t*)src + ch.offset,
-                             (size_t)ch.length, -1, -1, n_a});
-      }
-    } else if (P.kind == MP_PATH_GPU) {
-      Logi& L = ctx->logi[P.stage];
-      const int rp = L.phys;
-      // staging offset congruent to the source mod 16 keeps hop1 on the TMA path
-      stage_off[p] += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)L.stage + stage_off[p])) & 15u;
-      uint8_t* stage = L.stage + stage_off[p];
-      stage_off[p] += ch.length;
-      if (relay_sm) {
-        uint64_t t1 = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[sp].sms);
-        uint64_t t2 = auto_tile_bytes(ctx, path_bytes[p], ctx->phys[rp].sms);
-        uint32_t k1 = (uint32_t)ntiles_of((uint64_t)(uintptr_t)stage, ch.length, t1);
-        uint32_t k2 = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, t2);
+  uint32_t node = 0;  // logical node id of a chunk's first hop (graph.py:97-117), global
+  int lane_next = 0;
+  for (int t = 0; t < T; ++t) {
+    const Xfer& x = xs[t];
+    const auto& paths = x.paths;
+    const int np = (int)paths.size(), nc = (int)chunks[t].size();
+    const int sp = ctx->logi[x.sd].phys, dp = ctx->logi[x.dd].phys;
+    const uint64_t s0 = (uint64_t)(uintptr_t)x.src, d0 = (uint64_t)(uintptr_t)x.dst;
+    std::vector<int> lane_base(np, 0);
+    for (int p = 0; p < np; ++p) {
+      lane_base[p] = lane_next;
+      lane_next += paths[p].nhops;
+    }
+    std::vector<int> hop2_done_ev(nc, -1);  // host WAR: event recorded after hop2 of chunk
+    std::vector<int> host_chunk_of_seq;
+    uint64_t host_base = host_cursor;
+    for (int c = 0; c < nc; ++c) {
+      const mp_chunk& ch = chunks[t][c];
+      const mp_path& P = paths[ch.path_index];
+      const int p = ch.path_index;
+      const int g = chunk_base[t] + c;  // flag index, unique across the program
+      const uint64_t r2 = 2 * (uint64_t)ch.seq;
+      auto order = [&](uint64_t k) { return k * 64 + (uint64_t)t; };
+      const uint32_t n_a = node, n_b = node + 1;
+      node += (uint32_t)P.nhops;
+      const PathInfo& pi = info[t][p];
+      if (P.kind == MP_PATH_DIRECT) {
+        if (eng[t].direct_sm) {
+          int exec = o.pull ? dp : sp;
+          mpk::Tile proto{};
+          proto.node = n_a;
+          append_tiles(tiles[exec], order(r2), s0 + ch.offset, d0 + ch.offset, ch.length,
+                       auto_tile_bytes(ctx, pi.bytes, ctx->phys[exec].sms), proto);
+        } else {
+          e->ce.push_back(CeOp{sp, lane_base[p], (uint8_t*)x.dst + ch.offset,
+                               (const uint8_t*)x.src + ch.offset, (size_t)ch.length, -1, -1, n_a});
+        }
+      } else if (P.kind == MP_PATH_GPU) {
+        Logi& L = ctx->logi[P.stage];
+        const int rp = L.phys;
+        // staging offset congruent to the source mod 16 keeps hop1 on the TMA path
+        uint64_t& cur = stage_cursor[P.stage];
+        cur += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)L.stage + cur)) & 15u;
+        uint8_t* stage = L.stage + cur;
+        cur += ch.length;
+        if (eng[t].relay_sm) {
+          uint64_t t1 = auto_tile_bytes(ctx, pi.bytes, ctx->phys[sp].sms);
+          uint64_t t2 = auto_tile_bytes(ctx, pi.bytes, ctx->phys[rp].sms);
+          mpk::Tile h1{};
+          h1.signal = L.flags + g;
+          h1.node = n_a;
+          append_tiles(tiles[sp], order(r2), s0 + ch.offset, (uint64_t)(uintptr_t)stage, ch.length, t1,
+                       h1);
+          mpk::Tile h2{};
+          h2.wait = L.flags + g;
+          h2.pass = L.flags + L.flag_cap + g;
+          h2.wait_count = (uint32_t)ntiles_of((uint64_t)(uintptr_t)stage, ch.length, t1);
+          h2.pass_count = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, t2);
+          h2.flags = mpk::TILE_SRC_MUTABLE;
+          h2.node = n_b;
+          // hop2 of round r is queued after hop1 of round r+1 (overlap, no stall)
+          append_tiles(tiles[rp], order(r2 + 3), (uint64_t)(uintptr_t)stage, d0 + ch.offset, ch.length,
+                       t2, h2);
+        } else {
+          int ev = new_event(sp);
+          e->ce.push_back(CeOp{sp, lane_base[p], stage, (const uint8_t*)x.src + ch.offset,
+                               (size_t)ch.length, -1, ev, n_a});
+          e->ce.push_back(CeOp{rp, lane_base[p] + 1, (uint8_t*)x.dst + ch.offset, stage,
+                               (size_t)ch.length, ev, -1, n_b});
+        }
+      } else if (eng[t].host_sm) {
+        // host-staged by the SM kernels: hop1 tiles (src device) bulk-store into
+        // mapped pinned memory over PCIe, hop2 tiles (dst device) bulk-load it
+        // back after the chunk's flag (in dst memory) counts every hop1 tile.
+        Logi& L = ctx->logi[x.dd];
+        uint8_t* host_dev = nullptr;
+        CK(cudaHostGetDevicePointer((void**)&host_dev, ctx->host_stage, 0));
+        host_cursor += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)host_dev + host_cursor)) & 15u;
+        uint8_t* slot = host_dev + host_cursor;
+        host_cursor += ch.length;
+        const uint64_t th = std::min<uint64_t>(auto_tile_bytes(ctx, pi.bytes, ctx->phys[sp].sms),
+                                               kHostTileBytes);
         mpk::Tile h1{};
-        h1.signal = L.flags + c;
+        h1.signal = L.flags + g;
         h1.node = n_a;
-        append_tiles(tiles[sp], 2 * round, s0 + ch.offset, (uint64_t)(uintptr_t)stage, ch.length, t1, h1);
+        append_tiles(tiles[sp], order(r2), s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
         mpk::Tile h2{};
-        h2.wait = L.flags + c;
-        h2.pass = L.flags + L.flag_cap + c;
-        h2.wait_count = k1;
-        h2.pass_count = k2;
+        h2.wait = L.flags + g;
+        h2.pass = L.flags + L.flag_cap + g;
+        h2.wait_count = (uint32_t)ntiles_of((uint64_t)(uintptr_t)slot, ch.length, th);
+        h2.pass_count = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, th);
         h2.flags = mpk::TILE_SRC_MUTABLE;
         h2.node = n_b;
-        // hop2 of round r is queued after hop1 of round r+1 (overlap, no stall)
-        append_tiles(tiles[rp], 2 * round + 3, (uint64_t)(uintptr_t)stage, d0 + ch.offset, ch.length,
-                     t2, h2);
-      } else {
-        int ev = new_event(sp);
-        e->ce.push_back(CeOp{sp, lane_base[p], stage, (const uint8_t*)src + ch.offset, (size_t)ch.length,
-                             -1, ev, n_a});
-        e->ce.push_back(CeOp{rp, lane_base[p] + 1, (uint8_t*)dst + ch.offset, stage, (size_t)ch.length,
-                             ev, -1, n_b});
+        append_tiles(tiles[dp], order(r2 + 3), (uint64_t)(uintptr_t)slot, d0 + ch.offset, ch.length, th,
+                     h2);
+      } else {  // host-staged: D2H into pinned staging, H2D out of it (copy engines)
+        const int seq = ch.seq;
+        const int slots = eng[t].host_slots;
+        host_chunk_of_seq.push_back(c);
+        uint8_t* slot;
+        int war = -1;
+        if (slots < pi.count) {
+          slot = ctx->host_stage + host_base + (size_t)(seq % slots) * pi.nominal;
+          if (seq >= slots) war = hop2_done_ev[host_chunk_of_seq[seq - slots]];
+        } else {
+          slot = ctx->host_stage + host_cursor;
+          host_cursor += ch.length;
+        }
+        int ev1 = new_event(sp);
+        e->ce.push_back(CeOp{sp, lane_base[p], slot, (const uint8_t*)x.src + ch.offset, (size_t)ch.length,
+                             war, ev1, n_a});
+        int ev2 = -1;
+        if (slots < pi.count) {
+          ev2 = new_event(dp);
+          hop2_done_ev[c] = ev2;
+        }
+        e->ce.push_back(CeOp{dp, lane_base[p] + 1, (uint8_t*)x.dst + ch.offset, slot, (size_t)ch.length,
+                             ev1, ev2, n_b});
       }
-    } else if (host_sm) {
-      // host-staged by the SM kernels: hop1 tiles (src device) bulk-store into
-      // mapped pinned memory over PCIe, hop2 tiles (dst device) bulk-load it
-      // back after the chunk's flag (in dst memory) counts every hop1 tile.
-      Logi& L = ctx->logi[dst_dev];
-      uint8_t* host_dev = nullptr;
-      CK(cudaHostGetDevicePointer((void**)&host_dev, ctx->host_stage, 0));
-      stage_off[p] += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)host_dev + stage_off[p])) & 15u;
-      uint8_t* slot = host_dev + stage_off[p];
-      stage_off[p] += ch.length;
-      const uint64_t th = std::min<uint64_t>(auto_tile_bytes(ctx, path_bytes[p], ctx->phys[sp].sms),
-                                             kHostTileBytes);
-      uint32_t k1 = (uint32_t)ntiles_of((uint64_t)(uintptr_t)slot, ch.length, th);
-      uint32_t k2 = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, th);
-      mpk::Tile h1{};
-      h1.signal = L.flags + c;
-      h1.node = n_a;
-      append_tiles(tiles[sp], 2 * round, s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
-      mpk::Tile h2{};
-      h2.wait = L.flags + c;
-      h2.pass = L.flags + L.flag_cap + c;
-      h2.wait_count = k1;
-      h2.pass_count = k2;
-      h2.flags = mpk::TILE_SRC_MUTABLE;
-      h2.node = n_b;
-      append_tiles(tiles[dp], 2 * round + 3, (uint64_t)(uintptr_t)slot, d0 + ch.offset, ch.length, th, h2);
-    } else {  // host-staged: D2H into pinned staging, H2D out of it (copy engines)
-      int seq = ch.seq;
-      host_chunk_of_seq.push_back(c);
-      uint8_t* slot;
-      int war = -1;
-      if (host_slots < path_count[p]) {
-        slot = ctx->host_stage + (size_t)(seq % host_slots) * nominal[p];
-        if (seq >= host_slots) war = hop2_done_ev[host_chunk_of_seq[seq - host_slots]];
-      } else {
-        slot = ctx->host_stage + stage_off[p];
-        stage_off[p] += ch.length;
-      }
-      int ev1 = new_event(sp);
-      e->ce.push_back(CeOp{sp, lane_base[p], slot, (const uint8_t*)src + ch.offset, (size_t)ch.length, war,
-                           ev1, n_a});
-      int ev2 = -1;
-      if (host_slots < path_count[p]) {
-        ev2 = new_event(dp);
-        hop2_done_ev[c] = ev2;
-      }
-      e->ce.push_back(CeOp{dp, lane_base[p] + 1, (uint8_t*)dst + ch.offset, slot, (size_t)ch.length, ev1,
-                           ev2, n_b});
     }
+    for (int p = 0; p < np; ++p)  // reserve the slot ring of a WAR-reusing host path
+      if (paths[p].kind == MP_PATH_HOST && !eng[t].host_sm && eng[t].host_slots < info[t][p].count)
+        host_cursor = std::max<uint64_t>(host_cursor,
+                                         host_base + (uint64_t)eng[t].host_slots * info[t][p].nominal);
   }
   // upload one tile table per physical device
-  DeviceGuard g;
+  DeviceGuard dg;
   for (size_t ph = 0; ph < tiles.size(); ++ph) {
     auto& v = tiles[ph];
     if (v.empty()) continue;
@@ -516,14 +572,19 @@ Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* d
     Phys& P = ctx->phys[ph];
     pr.grid = (unsigned)std::min<uint64_t>(flat.size(), (uint64_t)P.sms * std::max(1, o.ctas_per_sm));
     bool waits = false;
-    for (const auto& t : flat) waits |= t.wait != nullptr;
+    for (const auto& tl : flat) waits |= tl.wait != nullptr;
     pr.nstatic = waits ? 0u : pr.grid;
     CK(cudaSetDevice(P.ordinal));
     CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile)));
+    e->progs.push_back(pr);  // owned by the entry from here (freed on error)
     CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
-    e->progs.push_back(pr);
   }
-  return e;
+  return e.release();
+}
+
+Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* dst, uint64_t size,
+                   int src_dev, int dst_dev, const mp_config& cfg) {
+  return build_entry_multi(ctx, key, {Xfer{src, dst, size, src_dev, dst_dev, {}}}, cfg);
 }
 
 // Enqueue the entry's work after `origin`, then make `origin` wait for it.
@@ -683,9 +744,10 @@ std::string make_key(const void* src, void* dst, uint64_t size, int sd, int dd, 
 // (graph.py:173-186).  Updates the lifecycle stats.
 Entry* lookup_entry(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int src_dev, int dst_dev,
                     const mp_config& cfg, cudaStream_t user,
-                    const std::function<Entry*(const std::string&)>& builder = nullptr) {
+                    const std::function<Entry*(const std::string&)>& builder = nullptr,
+                    const std::string* key_override = nullptr) {
   double t_start = now_us();
-  std::string key = make_key(src, dst, size, src_dev, dst_dev, cfg);
+  std::string key = key_override ? *key_override : make_key(src, dst, size, src_dev, dst_dev, cfg);
   mp_send_stats& st = ctx->stats;
   auto it = ctx->index.find(key);
   if (it != ctx->index.end()) {
@@ -1089,6 +1151,62 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
   st.nodes_logical = e->nodes_logical;
   st.nodes_physical = e->nodes_physical;
   st.kernels = (int)e->progs.size();
+  ctx->last_paths = e->paths;
+  ctx->last_chunks = e->chunks;
+  return MP_OK;
+  GUARD_END
+}
+
+int mp_send_many(mp_ctx* ctx, const mp_xfer* xfers, int32_t n, const mp_config* cfg, int32_t joint,
+                 void* stream) {
+  GUARD_BEGIN
+  if (!ctx || !cfg || !xfers || n < 1 || n > 64) return fail(MP_ERR_VALUE, "need 1..64 transfers");
+  if (!ctx->has_topo) return fail(MP_ERR_STATE, "context has no topology (mp_ctx_set_topology)");
+  if (ctx->group) return fail(MP_ERR_STATE, "group context: use mp_group_send");
+  std::vector<Xfer> xs;
+  std::string key = joint ? "J" : "I";
+  for (int i = 0; i < n; ++i) {
+    const mp_xfer& x = xfers[i];
+    if (x.src_dev < 0 || x.src_dev >= (int)ctx->logi.size() || x.dst_dev < 0 ||
+        x.dst_dev >= (int)ctx->logi.size())
+      return fail(MP_ERR_PLAN, "transfers run between accelerators");
+    if (x.size == 0) return fail(MP_ERR_CHUNK, "message size must be >= 1 byte, got 0");
+    if (!x.src || !x.dst) return fail(MP_ERR_VALUE, "null buffer");
+    xs.push_back(Xfer{x.src, x.dst, x.size, x.src_dev, x.dst_dev, {}});
+    key += make_key(x.src, x.dst, x.size, x.src_dev, x.dst_dev, *cfg);
+  }
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g;
+  cudaStream_t user = (cudaStream_t)stream;
+  Entry* e = lookup_entry(
+      ctx, xs[0].src, xs[0].dst, xs[0].size, xs[0].sd, xs[0].dd, *cfg, user,
+      [&](const std::string& k) {
+        if (joint) {  // channel-disjoint staging across the transfers (paths.py:210-242)
+          std::vector<std::pair<int, int>> tr;
+          for (auto& x : xs) tr.emplace_back(x.sd, x.dd);
+          int shared = 0;
+          auto sets = plan_contention_free_sets(ctx->topo, tr, *cfg, &shared);
+          for (size_t i = 0; i < xs.size(); ++i) xs[i].paths = sets[i];
+        }
+        return build_entry_multi(ctx, k, xs, *cfg);
+      },
+      &key);
+  mp_send_stats& st = ctx->stats;
+  Phys& S = ctx->phys[e->src_phys];
+  CK(cudaSetDevice(S.ordinal));
+  if (ctx->have_last && ctx->last_stream != stream) CK(cudaStreamWaitEvent(user, ctx->last_done, 0));
+  double t0 = now_us();
+  if (cfg->graph_mode && e->graph) CK(cudaGraphLaunch(e->exec, user));
+  else enqueue(ctx, e, user, false);
+  CK(cudaEventRecord(ctx->last_done, user));
+  ctx->have_last = true;
+  ctx->last_stream = stream;
+  st.launch_us = now_us() - t0;
+  st.graph_mode = cfg->graph_mode ? 1 : 0;
+  st.nodes_logical = e->nodes_logical;
+  st.nodes_physical = e->nodes_physical;
+  st.kernels = (int)e->progs.size();
+  st.ce_copies = (int)e->ce.size();
   ctx->last_paths = e->paths;
   ctx->last_chunks = e->chunks;
   return MP_OK;

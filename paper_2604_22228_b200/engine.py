@@ -189,6 +189,29 @@ class Engine:
         handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
         self.send_ptr(src.data_ptr(), dst.data_ptr(), nbytes, src_dev, dst_dev, config, handle)
 
+    def send_many(self, transfers, config: PathConfig | None = None, joint: bool = False,
+                  stream=None) -> None:
+        """Concurrent transfers as one program (windows, bidirectional flows,
+        ring halo exchanges): `transfers` = [(src, dst, nbytes, src_dev, dst_dev)]
+        with tensors; nbytes None = all of src.  joint=True picks channel-
+        disjoint staging devices (plan_contention_free, paths.py:210-242)."""
+        torch = _torch()
+        config = config or PathConfig.from_env()
+        arr = (_lib.mp_xfer * len(transfers))()
+        first = None
+        for i, (src, dst, nbytes, sd, dd) in enumerate(transfers):
+            n = src.numel() * src.element_size() if nbytes is None else nbytes
+            if n > src.numel() * src.element_size() or n > dst.numel() * dst.element_size():
+                raise ValueError("nbytes exceeds a buffer")
+            arr[i] = _lib.mp_xfer(src.data_ptr(), dst.data_ptr(), n, sd, dd)
+            first = first or src
+        if stream is None:
+            stream = torch.cuda.current_stream(first.device)
+        handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        cfg = config.abi()
+        check(lib.mp_send_many(self._ctx, arr, len(transfers), C.byref(cfg), int(joint),
+                               handle or None))
+
     def recv(self, dst, stream=None) -> None:
         """Single-process mode: `send` already wrote `dst` on the sender's
         stream; `recv` makes `stream` (default: current stream of dst's

@@ -37,7 +37,7 @@ def test_python_binding_covers_header():
 
 STRUCTS = ["mp_config", "mp_link", "mp_channel", "mp_hop", "mp_path", "mp_chunk", "mp_lane",
            "mp_lane_dep", "mp_node", "mp_edge", "mp_send_stats", "mp_engine_opts",
-           "mp_trace_rec"]
+           "mp_trace_rec", "mp_xfer"]
 
 
 def test_struct_layout_matches_c_compiler(tmp_path):
