@@ -204,7 +204,7 @@ class Engine:
             if n > src.numel() * src.element_size() or n > dst.numel() * dst.element_size():
                 raise ValueError("nbytes exceeds a buffer")
             arr[i] = _lib.mp_xfer(src.data_ptr(), dst.data_ptr(), n, sd, dd)
-            first = first or src
+            first = src if first is None else first
         if stream is None:
             stream = torch.cuda.current_stream(first.device)
         handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
