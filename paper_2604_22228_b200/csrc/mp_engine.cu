@@ -188,7 +188,7 @@ struct mp_ctx {
   cudaEvent_t last_done = nullptr;  // serialises sends issued on different streams
   void* last_stream = nullptr;
   bool have_last = false;
-  double kernel_ms = 0.0;
+  int timed_phys = -1;  // device whose kt0/kt1 events bracket the last timed kernel
   std::vector<std::pair<uint64_t, int>> size_policy;  // (max_bytes, direct engine)
   std::mutex mu;
 };
@@ -669,6 +669,7 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr 
     use(pr.phys, P.kstream);
     CK(cudaSetDevice(P.ordinal));
     bool t = timing && pr.phys == e->src_phys;
+    if (t) ctx->timed_phys = pr.phys;
     if (t) CK(cudaEventRecord(P.kt0, P.kstream));
     launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic,
                     tr ? tr->stamps[pr.phys] : nullptr);
@@ -1379,7 +1380,8 @@ int mp_kernel_time_ms(const mp_ctx* ctx, double* ms) {
   GUARD_BEGIN
   if (!ctx || !ms) return fail(MP_ERR_VALUE, "null argument");
   DeviceGuard g;
-  const Phys& S = ctx->phys[0];
+  if (ctx->timed_phys < 0) return fail(MP_ERR_STATE, "no timed kernel yet (streamed-mode SM send)");
+  const Phys& S = ctx->phys[ctx->timed_phys];
   CK(cudaSetDevice(S.ordinal));
   float f = 0.f;
   CK(cudaEventSynchronize(S.kt1));

@@ -315,6 +315,31 @@ class Engine:
         link, host = self.probe_bandwidths(nbytes, iters)
         return mesh_text(name, n, link, 1, 2e-6, host, 10e-6, "full")
 
+    def probe_node(self, nbytes: int = 256 << 20, iters: int = 5, name: str = "probed") -> str:
+        """Measure every accelerator pair and host link of the context and
+        write a reference-schema `.topo` (SURVEY §8c protocol: bandwidths with
+        repr(), sublinks 1, so the planner parses back the identical doubles).
+        Pairs on the same physical devices are measured once."""
+        n = len(self.topology.accelerators)
+        pair_bw: dict[tuple[int, int], float] = {}
+        host_bw: dict[int, float] = {}
+        lines = [f"name {name}", "[device]"] + [f"{i} accelerator" for i in range(n)] + ["[link]"]
+        for a in range(n):
+            for b in range(a + 1, n):
+                key = (self.device_map[a], self.device_map[b])
+                if key not in pair_bw:
+                    m = self.measure_paths(a, b, nbytes, iters)
+                    pair_bw[key] = max(m["direct_sm"], m["direct_ce"]) * 1e9
+                lines.append(f"{a} {b} {pair_bw[key]!r} 2e-06 full 1")
+        lines.append("[hostlink]")
+        for d in range(n):
+            phys = self.device_map[d]
+            if phys not in host_bw:
+                m = self.measure_paths(d, d, nbytes, iters)
+                host_bw[phys] = min(m["d2h"], m["h2d"]) * 1e9
+            lines.append(f"{d} {host_bw[phys]!r} 1e-05 full")
+        return "\n".join(lines) + "\n"
+
     def probe_bandwidths(self, nbytes: int = 256 << 20, iters: int = 5,
                          host_bytes: int = 8 << 20) -> tuple[float, float]:
         """(link, host) bytes/s for the planner's `.topo`.

@@ -173,3 +173,34 @@ def test_streams_and_events_order_with_user_work():
             total = dst.sum(dtype=torch.int64)
             assert int(total) == v * n
     eng.close()
+
+
+def test_full_size_512mib_multipath_bytes_exact():
+    """BASELINE size: 512 MiB + 7 over direct + 2 relays + host, compared on
+    the device (size-independent property: dst == src everywhere)."""
+    from paper_2604_22228_b200 import PathConfig
+    eng, _ = _engine(4)
+    n = 512 * MiB + 7
+    src = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0",
+                        generator=torch.Generator(device="cuda:0").manual_seed(20261017))
+    dst = torch.bitwise_not(src)
+    for graph in (False, True):
+        cfg = PathConfig(num_gpu_paths=3, host_path_enabled=True, max_chunks=8, graph_mode=graph)
+        eng.send(src, dst, n, cfg, src_dev=0, dst_dev=1)
+        eng.sync()
+        assert torch.equal(src, dst)
+        dst.bitwise_not_()
+    eng.close()
+
+
+def test_probe_node_writes_a_plannable_topology():
+    import paper_2604_22228_b200 as mp
+    eng, _ = _engine(3)
+    text = eng.probe_node(64 * MiB, 3, name="probed3")
+    topo = mp.load_topology(text)
+    assert topo.name == "probed3" and len(topo.accelerators) == 3
+    assert all(ch.bandwidth > 1e9 for ch in topo.channels())
+    ps = mp.plan_paths(topo, topo.device(0), topo.device(1),
+                       mp.PathConfig(num_gpu_paths=2, host_path_enabled=True))
+    assert abs(sum(p.share for p in ps.paths) - 1.0) < 1e-12
+    eng.close()
