@@ -333,14 +333,17 @@ def run_ours(args, rank, world):
     single_t = time_sends(torch, eng, PathConfig(max_chunks=1, graph_mode=True), src, dst,
                           size, args.steps * 4, 3, stream)
 
-    # 3. dominant kernel: transfer_kernel duration (events on its stream, streamed mode)
+    # 3. dominant kernel: transfer_kernel average launch duration — CUDA events
+    #    on its own stream around back-to-back launches of this send's program
+    #    (and, for reference, around single streamed-mode launches)
     cfg_s = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=args.chunks,
                        graph_mode=False)
+    kms = eng.kernel_bench(src, dst, size, cfg_s, 0, 1, reps=max(10, args.steps))
     ktimes = []
-    for _ in range(max(4, args.steps // 2)):
+    for _ in range(5):
         eng.send(src, dst, size, cfg_s, stream=stream, src_dev=0, dst_dev=1)
         ktimes.append(eng.kernel_time_ms())
-    kms = statistics.mean(ktimes[1:])
+    kms_single = statistics.median(ktimes[1:])
     k_alg_bytes = 2 * direct_bytes  # HBM read + write of the direct share
     achieved = k_alg_bytes / (kms / 1e3) / 1e9
     pcie = min(m["d2h"], m["h2d"])
@@ -411,6 +414,7 @@ def run_ours(args, rank, world):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "kernel": "mpk::transfer_kernel<1,8> (TMA bulk ring)", "kernel_ms": kms,
+                     "kernel_ms_single_launch": kms_single,
                      "alg_bytes_per_launch": k_alg_bytes, "peak_kind": peak_kind,
                      "traffic_source": ncu and ncu.get("source")},
         "path_roofline": {"R_gbs": path_roofline, "frac": value / path_roofline,

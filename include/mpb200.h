@@ -337,13 +337,21 @@ int mp_sync(mp_ctx* ctx);
  * type between src and dst and writes GB/s (1e9 B/s): out[0] = direct by the
  * SM transfer kernel, out[1] = D2H, out[2] = H2D, out[3] = direct by a CE
  * copy; with cap >= 6 also out[4] = D2H and H2D concurrently (per direction)
- * and out[5] = the host-staged path as executed (8 pipelined chunks). */
+ * and out[5] = the host-staged path as executed (8 pipelined chunks); with
+ * cap >= 8 also out[6] / out[7] = the SM transfer kernel writing to / reading
+ * from mapped pinned host memory (the SM variant of the host hops). */
 int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t bytes,
                      int32_t iters, double* out_gbps, int32_t cap);
 
-/* Device time of the copy kernels launched by the last `n` sends on the src
- * device (CUDA events around each kernel, streamed mode only). */
+/* Device time of the transfer kernel of the last streamed-mode send (CUDA
+ * events on its stream around that one launch, launch latency included). */
 int mp_kernel_time_ms(const mp_ctx* ctx, double* ms);
+/* Average duration of the src device's transfer kernel for this transfer's
+ * program over `reps` back-to-back launches between two CUDA events on its
+ * stream (launch gaps amortised): the roofline denominator.  Only the kernel
+ * runs (copy-engine lanes are not enqueued); synchronous. */
+int mp_kernel_bench(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_dev,
+                    int32_t dst_dev, const mp_config* cfg, int32_t reps, double* ms_per_launch);
 
 /* ---- CUDA IPC (multi-process mode) --------------------------------------- */
 #define MP_IPC_HANDLE_BYTES 64

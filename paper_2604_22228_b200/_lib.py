@@ -170,6 +170,8 @@ SIGNATURES = {
     "mp_sync": (C.c_int, [_vp]),
     "mp_measure_paths": (C.c_int, [_vp, _i32, _i32, _u64, _i32, P(C.c_double), _i32]),
     "mp_kernel_time_ms": (C.c_int, [_vp, P(C.c_double)]),
+    "mp_kernel_bench": (C.c_int, [_vp, _vp, _vp, _u64, _i32, _i32, P(mp_config), _i32,
+                                  P(C.c_double)]),
     "mp_ipc_export": (C.c_int, [_vp, _i32, P(C.c_uint8), P(_u64)]),
     "mp_ipc_import": (C.c_int, [P(C.c_uint8), _i32, P(_vp)]),
     "mp_ipc_close": (C.c_int, [_vp, _i32]),

@@ -1391,6 +1391,41 @@ int mp_kernel_time_ms(const mp_ctx* ctx, double* ms) {
   GUARD_END
 }
 
+int mp_kernel_bench(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_dev,
+                    int32_t dst_dev, const mp_config* cfg, int32_t reps, double* ms_per_launch) {
+  GUARD_BEGIN
+  if (!ctx || !cfg || !ms_per_launch || reps < 1) return fail(MP_ERR_VALUE, "bad arguments");
+  if (!ctx->has_topo) return fail(MP_ERR_STATE, "context has no topology (mp_ctx_set_topology)");
+  if (ctx->group) return fail(MP_ERR_STATE, "group context");
+  if (src_dev < 0 || src_dev >= (int)ctx->logi.size() || dst_dev < 0 || dst_dev >= (int)ctx->logi.size())
+    return fail(MP_ERR_PLAN, "transfers run between accelerators");
+  if (!src || !dst || size == 0) return fail(MP_ERR_VALUE, "null buffer or empty message");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g;
+  mp_config c = *cfg;
+  c.graph_mode = 0;
+  Phys& S0 = ctx->phys[ctx->logi[src_dev].phys];
+  Entry* e = lookup_entry(ctx, src, dst, size, src_dev, dst_dev, c, S0.capture);
+  const Program* pr = nullptr;
+  for (const auto& p : e->progs)
+    if (p.phys == e->src_phys) pr = &p;
+  if (!pr) return fail(MP_ERR_STATE, "no SM transfer kernel on the source device for this transfer");
+  Phys& S = ctx->phys[e->src_phys];
+  CK(cudaSetDevice(S.ordinal));
+  CK(cudaDeviceSynchronize());
+  launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic);  // warm
+  CK(cudaEventRecord(S.kt0, S.kstream));
+  for (int i = 0; i < reps; ++i)
+    launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic);
+  CK(cudaEventRecord(S.kt1, S.kstream));
+  CK(cudaEventSynchronize(S.kt1));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, S.kt0, S.kt1));
+  *ms_per_launch = ms / reps;
+  return MP_OK;
+  GUARD_END
+}
+
 int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t bytes, int32_t iters,
                      double* out_gbps, int32_t cap) {
   GUARD_BEGIN
@@ -1408,7 +1443,7 @@ int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t byt
   CK(cudaMemset(a, 1, bytes));
   CK(cudaSetDevice(D.ordinal));
   CK(cudaMalloc(&b, bytes));
-  CK(cudaHostAlloc((void**)&h, bytes, cudaHostAllocPortable));
+  CK(cudaHostAlloc((void**)&h, bytes, cudaHostAllocPortable | cudaHostAllocMapped));
   auto time_it = [&](Phys& P, auto&& fn) {
     CK(cudaSetDevice(P.ordinal));
     fn(P.kstream);  // warm-up
@@ -1441,6 +1476,35 @@ int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t byt
   out_gbps[1] = time_it(S, [&](cudaStream_t s) { cudaMemcpyAsync(h, a, bytes, cudaMemcpyDeviceToHost, s); });
   out_gbps[2] = time_it(D, [&](cudaStream_t s) { cudaMemcpyAsync(b, h, bytes, cudaMemcpyHostToDevice, s); });
   out_gbps[3] = time_it(S, [&](cudaStream_t s) { cudaMemcpyAsync(b, a, bytes, cudaMemcpyDefault, s); });
+  if (cap >= 8) {
+    // out[6] / out[7]: the SM transfer kernel writing to / reading from mapped
+    // pinned host memory over PCIe (the SM variant of the host-staged hops)
+    uint8_t* hd = nullptr;
+    CK(cudaHostGetDevicePointer((void**)&hd, h, 0));
+    auto sm_copy = [&](uint8_t* from, uint8_t* to) {
+      std::vector<mpk::Tile> ft;
+      uint64_t tl = std::min<uint64_t>(auto_tile_bytes(ctx, bytes, S.sms), kHostTileBytes);
+      for (uint64_t o = 0; o < bytes; o += tl) {
+        mpk::Tile t{};
+        t.src = (uint64_t)(uintptr_t)(from + o);
+        t.dst = (uint64_t)(uintptr_t)(to + o);
+        t.len = std::min(tl, bytes - o);
+        ft.push_back(t);
+      }
+      mpk::Tile* d = nullptr;
+      CK(cudaSetDevice(S.ordinal));
+      CK(cudaMalloc(&d, ft.size() * sizeof(mpk::Tile)));
+      CK(cudaMemcpy(d, ft.data(), ft.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
+      unsigned gr = (unsigned)std::min<uint64_t>(ft.size(), (uint64_t)S.sms * ctx->opts.ctas_per_sm);
+      double r = time_it(S, [&](cudaStream_t s) {
+        launch_transfer(ctx->opts, gr, s, d, (unsigned)ft.size(), S.ctl, gr);
+      });
+      cudaFree(d);
+      return r;
+    };
+    out_gbps[6] = sm_copy(a, hd);
+    out_gbps[7] = sm_copy(hd, b);
+  }
   if (cap >= 6) {
     // out[4]: D2H and H2D running at the same time (full duplex), per direction
     // out[5]: the host-staged path as the engine runs it: 8 pipelined chunks,

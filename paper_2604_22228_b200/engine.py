@@ -286,6 +286,18 @@ class Engine:
         check(lib.mp_kernel_time_ms(self._ctx, C.byref(ms)))
         return ms.value
 
+    def kernel_bench(self, src, dst, nbytes: int | None = None, config: PathConfig | None = None,
+                     src_dev: int = 0, dst_dev: int = 1, reps: int = 20) -> float:
+        """Milliseconds per launch of this transfer's source-device kernel over
+        `reps` back-to-back launches (`mp_kernel_bench`)."""
+        config = config or PathConfig()
+        nbytes = src.numel() * src.element_size() if nbytes is None else nbytes
+        cfg = config.abi()
+        ms = C.c_double()
+        check(lib.mp_kernel_bench(self._ctx, src.data_ptr(), dst.data_ptr(), nbytes, src_dev,
+                                  dst_dev, C.byref(cfg), reps, C.byref(ms)))
+        return ms.value
+
     def peer_matrix(self) -> list[list[int]]:
         n = len(set(self.device_map))
         arr = (C.c_int32 * (n * n))()
@@ -298,10 +310,10 @@ class Engine:
         the SM transfer kernel and a CE copy on the direct route, D2H and H2D
         alone, both at once (per direction), and the host-staged path run as
         the engine runs it (8 pipelined chunks, event handoff)."""
-        out = (C.c_double * 6)()
-        check(lib.mp_measure_paths(self._ctx, src_dev, dst_dev, nbytes, iters, out, 6))
+        out = (C.c_double * 8)()
+        check(lib.mp_measure_paths(self._ctx, src_dev, dst_dev, nbytes, iters, out, 8))
         return {"direct_sm": out[0], "d2h": out[1], "h2d": out[2], "direct_ce": out[3],
-                "duplex": out[4], "host_staged": out[5]}
+                "duplex": out[4], "host_staged": out[5], "sm_d2h": out[6], "sm_h2d": out[7]}
 
     def probe_topology(self, nbytes: int = 256 << 20, iters: int = 5,
                        name: str = "probed") -> str:
