@@ -421,6 +421,7 @@ def run_ours(args, rank, world):
                           "hbm_copy_gbs": hbm_peak / 2, "pcie_gbs": pcie, "probe": m,
                           "direct_bytes": direct_bytes, "host_bytes": host_bytes,
                           "host_bw_calibrated": host_bw, "link_bw": link_bw,
+                          "host_engine": "sm" if eng.options()["host_engine"] == 0 else "ce",
                           "calibration": trials,
                           "single_path_sm_gbs": size / single_t / 1e9},
         "cpu_baseline": cpu,
@@ -475,11 +476,11 @@ def run_sweep(torch, eng, topo_text, dev, stream):
         row["tuned"] = size / time_sends(torch, auto, table.config_for(size), src, dst, size,
                                          steps, warm, stream) / 1e9
         row["tuned_point"] = [best.gpu_paths, best.host, best.max_chunks,
-                              next(e for b, e in rules if size <= b)]
+                              *next(r[1:] for r in rules if size <= r[0])]
         rows.append(row)
     ce.close()
     auto.close()
-    return rows, {"table_csv": table.to_csv(), "direct_engine_policy": rules}
+    return rows, {"table_csv": table.to_csv(), "engine_policy": rules}
 
 
 def run_lifecycle(torch, eng, dev, stream):

@@ -268,12 +268,14 @@ void mp_ctx_destroy(mp_ctx* ctx);
 int mp_ctx_set_topology(mp_ctx* ctx, const mp_topology* topo);
 int mp_ctx_set_engine(mp_ctx* ctx, const mp_engine_opts* opts);
 int mp_ctx_get_engine(const mp_ctx* ctx, mp_engine_opts* opts);
-/* Per-message-size choice of the direct-path mechanism, from measurement
- * (tuner.tune_engines): a message of S bytes uses direct_engine[i] for the
- * first i with S <= max_bytes[i]; sizes past the table (or n = 0) use
- * opts.direct_engine. */
+/* Per-message-size choice of the direct-path and host-path mechanisms, from
+ * measurement (tuner.tune_engines): a message of S bytes uses
+ * direct_engine[i] / host_engine[i] for the first i with S <= max_bytes[i]
+ * (host_engine may be NULL: keep opts.host_engine); sizes past the table (or
+ * n = 0) use opts. */
 int mp_ctx_set_size_policy(mp_ctx* ctx, const uint64_t* max_bytes,
-                           const int32_t* direct_engine, int32_t n);
+                           const int32_t* direct_engine, const int32_t* host_engine,
+                           int32_t n);
 int mp_ctx_peer_matrix(const mp_ctx* ctx, int32_t* out, int32_t cap);
 
 /* The multi-path transfer: size bytes from src (on logical src_dev) to dst

@@ -157,7 +157,7 @@ SIGNATURES = {
     "mp_ctx_set_topology": (C.c_int, [_vp, _vp]),
     "mp_ctx_set_engine": (C.c_int, [_vp, P(mp_engine_opts)]),
     "mp_ctx_get_engine": (C.c_int, [_vp, P(mp_engine_opts)]),
-    "mp_ctx_set_size_policy": (C.c_int, [_vp, P(C.c_uint64), P(_i32), _i32]),
+    "mp_ctx_set_size_policy": (C.c_int, [_vp, P(C.c_uint64), P(_i32), P(_i32), _i32]),
     "mp_ctx_peer_matrix": (C.c_int, [_vp, P(_i32), _i32]),
     "mp_send": (C.c_int, [_vp, _vp, _vp, _u64, _i32, _i32, P(mp_config), _vp]),
     "mp_wait": (C.c_int, [_vp, _vp]),

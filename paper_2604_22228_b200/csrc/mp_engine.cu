@@ -189,7 +189,11 @@ struct mp_ctx {
   void* last_stream = nullptr;
   bool have_last = false;
   int timed_phys = -1;  // device whose kt0/kt1 events bracket the last timed kernel
-  std::vector<std::pair<uint64_t, int>> size_policy;  // (max_bytes, direct engine)
+  struct SizeRule {
+    uint64_t max_bytes;
+    int direct, host;  // MP_ENGINE_*, host -1 = opts.host_engine
+  };
+  std::vector<SizeRule> size_policy;
   std::mutex mu;
 };
 
@@ -398,14 +402,15 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
     }
     // engines per path type for this message size (measured policy)
     const bool sm_ok = xs[t].size >= (uint64_t)o.sm_min_bytes;
-    int direct_engine = o.direct_engine;
+    int direct_engine = o.direct_engine, host_engine = o.host_engine;
     for (const auto& rule : ctx->size_policy)
-      if (xs[t].size <= rule.first) {
-        direct_engine = rule.second;
+      if (xs[t].size <= rule.max_bytes) {
+        direct_engine = rule.direct;
+        if (rule.host >= 0) host_engine = rule.host;
         break;
       }
     eng[t] = Engines{direct_engine == MP_ENGINE_SM && sm_ok, o.relay_engine == MP_ENGINE_SM && sm_ok,
-                     o.host_engine == MP_ENGINE_SM && sm_ok, 0};
+                     host_engine == MP_ENGINE_SM && sm_ok, 0};
     for (size_t p = 0; p < paths.size(); ++p) {
       const PathInfo& pi = info[t][p];
       if (paths[p].kind == MP_PATH_GPU) {
@@ -453,7 +458,11 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
       const int p = ch.path_index;
       const int g = chunk_base[t] + c;  // flag index, unique across the program
       const uint64_t r2 = 2 * (uint64_t)ch.seq;
-      auto order = [&](uint64_t k) { return k * 64 + (uint64_t)t; };
+      // queue position: round-robin rounds, transfers interleaved; slot 0 is
+      // reserved for the SM host path's hop1 tiles, which go first so their
+      // latency-bound PCIe writes overlap the whole HBM/NVLink stream instead
+      // of forming a tail
+      auto order = [&](uint64_t k) { return (k + 1) * 64 + (uint64_t)t; };
       const uint32_t n_a = node, n_b = node + 1;
       node += (uint32_t)P.nhops;
       const PathInfo& pi = info[t][p];
@@ -516,7 +525,7 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
         mpk::Tile h1{};
         h1.signal = L.flags + g;
         h1.node = n_a;
-        append_tiles(tiles[sp], order(r2), s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
+        append_tiles(tiles[sp], (uint64_t)t, s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
         mpk::Tile h2{};
         h2.wait = L.flags + g;
         h2.pass = L.flags + L.flag_cap + g;
@@ -524,7 +533,11 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
         h2.pass_count = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, th);
         h2.flags = mpk::TILE_SRC_MUTABLE;
         h2.node = n_b;
-        append_tiles(tiles[dp], order(r2 + 3), (uint64_t)(uintptr_t)slot, d0 + ch.offset, ch.length, th,
+        // every hop2 tile queues after the first two rounds: its hop1 tiles were
+        // front-loaded, so it rarely waits, and no PCIe-latency tile is left
+        // for the tail of the HBM/NVLink stream
+        append_tiles(tiles[dp], order(std::min<uint64_t>(r2 + 3, 3)), (uint64_t)(uintptr_t)slot,
+                     d0 + ch.offset, ch.length, th,
                      h2);
       } else {  // host-staged: D2H into pinned staging, H2D out of it (copy engines)
         const int seq = ch.seq;
@@ -1080,17 +1093,18 @@ int mp_ctx_set_engine(mp_ctx* ctx, const mp_engine_opts* o) {
 }
 
 int mp_ctx_set_size_policy(mp_ctx* ctx, const uint64_t* max_bytes, const int32_t* direct_engine,
-                           int32_t n) {
+                           const int32_t* host_engine, int32_t n) {
   GUARD_BEGIN
   if (!ctx || n < 0 || (n > 0 && (!max_bytes || !direct_engine)))
     return fail(MP_ERR_VALUE, "bad size policy arguments");
-  std::vector<std::pair<uint64_t, int>> rules;
+  std::vector<mp_ctx::SizeRule> rules;
+  auto ok = [](int e) { return e == MP_ENGINE_SM || e == MP_ENGINE_CE; };
   for (int i = 0; i < n; ++i) {
-    if (direct_engine[i] != MP_ENGINE_SM && direct_engine[i] != MP_ENGINE_CE)
+    if (!ok(direct_engine[i]) || (host_engine && !ok(host_engine[i])))
       return fail(MP_ERR_VALUE, "unknown engine in size policy");
     if (i > 0 && max_bytes[i] <= max_bytes[i - 1])
       return fail(MP_ERR_VALUE, "size policy bounds must increase");
-    rules.emplace_back(max_bytes[i], direct_engine[i]);
+    rules.push_back(mp_ctx::SizeRule{max_bytes[i], direct_engine[i], host_engine ? host_engine[i] : -1});
   }
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;

@@ -139,13 +139,18 @@ class Engine:
             o.sm_min_bytes = sm_min_bytes
         check(lib.mp_ctx_set_engine(self._ctx, C.byref(o)))
 
-    def set_size_policy(self, rules: list[tuple[int, str]]) -> None:
-        """[(max_bytes, "sm"|"ce"), ...] increasing: the direct-path mechanism
-        per message size (from `tuner.tune_engines`); [] restores the default."""
+    def set_size_policy(self, rules: list[tuple]) -> None:
+        """[(max_bytes, direct, host), ...] with increasing max_bytes and
+        "sm"|"ce" mechanisms (host may be omitted/None: keep the default) —
+        the per-size choice from `tuner.tune_engines`; [] restores defaults."""
         n = len(rules)
-        mx = (C.c_uint64 * max(1, n))(*[int(b) for b, _ in rules])
-        en = (C.c_int32 * max(1, n))(*[ENGINES[e] for _, e in rules])
-        check(lib.mp_ctx_set_size_policy(self._ctx, mx, en, n))
+        mx = (C.c_uint64 * max(1, n))(*[int(r[0]) for r in rules])
+        en = (C.c_int32 * max(1, n))(*[ENGINES[r[1]] for r in rules])
+        hosts = [r[2] if len(r) > 2 else None for r in rules]
+        he = None
+        if any(h is not None for h in hosts):
+            he = (C.c_int32 * max(1, n))(*[ENGINES[h] if h else ENGINES["ce"] for h in hosts])
+        check(lib.mp_ctx_set_size_policy(self._ctx, mx, en, he, n))
         self.size_policy = list(rules)
 
     def options(self) -> dict:

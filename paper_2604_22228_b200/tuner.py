@@ -136,48 +136,67 @@ def tune(engine, sizes: list[int], grid: list[GridPoint] | None = None,
     return TuningTable(engine.topology.name, entries)
 
 
-def tune_engines(engine, sizes: list[int], reps: int = 10,
-                 mode: str = GRAPH_MODE) -> tuple[list[tuple[int, str]], list[dict]]:
-    """Measure the direct path by the SM transfer kernel and by a copy-engine
-    copy at every size; return the per-size policy for
-    `Engine.set_size_policy` (boundaries at the geometric mid-points between
-    tuned sizes) and the raw trials."""
+def tune_engines(engine, sizes: list[int], reps: int = 10, mode: str = GRAPH_MODE,
+                 host_chunks: int = 2) -> tuple[list[tuple[int, str, str]], list[dict]]:
+    """Measure, at every size, the direct path by the SM transfer kernel vs a
+    copy-engine copy (single path), then — with the winning direct mechanism —
+    the host-staged path by the SM kernels (mapped pinned memory) vs copy
+    engines (direct + host, `host_chunks` chunks).  Returns the per-size
+    policy [(max_bytes, direct, host)] for `Engine.set_size_policy`
+    (boundaries at the geometric mid-points between tuned sizes) and the raw
+    trials."""
     import torch
     sizes = sorted(sizes)
     dev = engine.device_map[0]
     big = torch.empty(sizes[-1], dtype=torch.uint8, device=f"cuda:{dev}")
     out = torch.empty_like(big)
     stream = torch.cuda.Stream(device=dev)
-    cfg = PathConfig(max_chunks=1, graph_mode=mode == GRAPH_MODE)
+    graph = mode == GRAPH_MODE
     saved = engine.options()
     engine.set_size_policy([])
     trials = []
-    for eng_name in ("sm", "ce"):
-        engine.configure(direct=eng_name)
+    single = PathConfig(max_chunks=1, graph_mode=graph)
+    for name in ("sm", "ce"):
+        engine.configure(direct=name)
         for s in sizes:
-            t = measure_makespan(engine, cfg, s, big[:s], out[:s], stream, reps)
-            trials.append({"bytes": s, "engine": eng_name, "seconds": t})
-    engine.configure(direct="sm" if saved["direct_engine"] == 0 else "ce")
-    best = {}
-    for s in sizes:
-        ts = {t["engine"]: t["seconds"] for t in trials if t["bytes"] == s}
-        best[s] = "sm" if ts["sm"] <= ts["ce"] else "ce"
-    rules: list[tuple[int, str]] = []
+            t = measure_makespan(engine, single, s, big[:s], out[:s], stream, reps)
+            trials.append({"bytes": s, "path": "direct", "engine": name, "seconds": t})
+
+    def pick(path, s):
+        ts = {t["engine"]: t["seconds"] for t in trials if t["bytes"] == s and t["path"] == path}
+        return "sm" if ts["sm"] <= ts["ce"] else "ce"
+    direct = {s: pick("direct", s) for s in sizes}
+    multi = PathConfig(1, True, host_chunks, graph)
+    for name in ("sm", "ce"):
+        engine.configure(host=name)
+        for s in sizes:
+            engine.set_size_policy([(2**63 - 1, direct[s], name)])
+            t = measure_makespan(engine, multi, s, big[:s], out[:s], stream, reps)
+            trials.append({"bytes": s, "path": "host", "engine": name, "seconds": t})
+    engine.set_size_policy([])
+    engine.configure(direct="sm" if saved["direct_engine"] == 0 else "ce",
+                     host="sm" if saved["host_engine"] == 0 else "ce")
+    rules: list[tuple[int, str, str]] = []
     for i, s in enumerate(sizes):
+        choice = (direct[s], pick("host", s))
         bound = int(math.sqrt(s * sizes[i + 1])) if i + 1 < len(sizes) else 2**63 - 1
-        if rules and rules[-1][1] == best[s]:
-            rules[-1] = (bound, best[s])
+        if rules and rules[-1][1:] == choice:
+            rules[-1] = (bound, *choice)
         else:
-            rules.append((bound, best[s]))
+            rules.append((bound, *choice))
     engine.clear_cache()
     return rules, trials
 
 
 def calibrate_host_bandwidth(engine, link_bw: float, size: int, max_chunks: int,
                              candidates: list[float] | None = None, reps: int = 10,
-                             name: str = "calibrated") -> tuple[float, Topology, list]:
-    """Pick the host-link bandwidth for the `.topo` that maximises the measured
-    direct+host throughput at `size`; returns (host_bw, topology, trials)."""
+                             name: str = "calibrated",
+                             host_engines: tuple[str, ...] = ("ce", "sm")
+                             ) -> tuple[float, Topology, list]:
+    """Pick the host-link bandwidth for the `.topo` (and the host-path
+    mechanism) that maximise the measured direct+host throughput at `size`.
+    Leaves `engine` on the winning topology and host mechanism; returns
+    (host_bw, topology, trials) with trials = [(engine, host_bw, GB/s)]."""
     import torch
     n = len(engine.topology.accelerators)
     if candidates is None:
@@ -189,12 +208,15 @@ def calibrate_host_bandwidth(engine, link_bw: float, size: int, max_chunks: int,
     cfg = PathConfig(1, True, max_chunks, True)
     trials = []
     best = None
-    for bw in candidates:
-        topo = load_topology(mesh_text(name, n, link_bw, 1, 2e-6, bw, 1e-5, "full"))
-        engine.set_topology(topo)
-        t = measure_makespan(engine, cfg, size, src, dst, stream, reps)
-        trials.append((bw, size / t / 1e9))
-        if best is None or t < best[0]:
-            best = (t, bw, topo)
+    for host in host_engines:
+        engine.configure(host=host)
+        for bw in candidates:
+            topo = load_topology(mesh_text(name, n, link_bw, 1, 2e-6, bw, 1e-5, "full"))
+            engine.set_topology(topo)
+            t = measure_makespan(engine, cfg, size, src, dst, stream, reps)
+            trials.append((host, bw, size / t / 1e9))
+            if best is None or t < best[0]:
+                best = (t, bw, topo, host)
+    engine.configure(host=best[3])
     engine.set_topology(best[2])
     return best[1], best[2], trials

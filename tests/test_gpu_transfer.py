@@ -74,11 +74,12 @@ def test_direct_sizes(size, graph, copy):
     eng.close()
 
 
-@pytest.mark.parametrize("direct", ["sm", "ce"])
+@pytest.mark.parametrize("direct,host", [("sm", "ce"), ("ce", "ce"), ("sm", "sm")])
 @pytest.mark.parametrize("k", [1, 2, 4, 8, 16, 32])
-def test_config1_direct_plus_host_64mib(direct, k):
-    """BASELINE config 1: 64 MiB over direct + host-staged, K chunks per path."""
-    eng, text = _engine(2, direct=direct)
+def test_config1_direct_plus_host_64mib(direct, host, k):
+    """BASELINE config 1: 64 MiB over direct + host-staged, K chunks per path
+    (host hops by copy engines or by the SM kernels over mapped memory)."""
+    eng, text = _engine(2, direct=direct, host=host)
     st = _check(eng, text, 64 * MiB, host=True, chunks=k, graph=True)
     assert st.nodes_logical == sum(1 if p == 0 else 2 for p, *_ in
                                    op.make_chunk_plan(
