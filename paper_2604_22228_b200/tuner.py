@@ -91,18 +91,24 @@ class TuningTable:
 
 
 def measure_makespan(engine, config: PathConfig, size: int, src, dst, stream,
-                     reps: int = 10, warmup: int = 2) -> float:
-    """Seconds per transfer: CUDA events around `reps` back-to-back sends."""
+                     reps: int = 10, warmup: int = 5, trials: int = 3) -> float:
+    """Seconds per transfer: CUDA events around `reps` back-to-back sends,
+    best of `trials`.  The warm-up replays matter: the first launches of a
+    freshly instantiated graph are several times slower than steady state."""
     import torch
     for _ in range(warmup):
         engine.send(src, dst, size, config, stream=stream, src_dev=0, dst_dev=1)
+    best = None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(reps):
-        engine.send(src, dst, size, config, stream=stream, src_dev=0, dst_dev=1)
-    e1.record(stream)
-    e1.synchronize()
-    return e0.elapsed_time(e1) / 1e3 / reps
+    for _ in range(trials):
+        e0.record(stream)
+        for _ in range(reps):
+            engine.send(src, dst, size, config, stream=stream, src_dev=0, dst_dev=1)
+        e1.record(stream)
+        e1.synchronize()
+        t = e0.elapsed_time(e1) / 1e3 / reps
+        best = t if best is None else min(best, t)
+    return best
 
 
 def tune(engine, sizes: list[int], grid: list[GridPoint] | None = None,
