@@ -1,0 +1,208 @@
+"""Measured benchmark harness in the reference's schema.
+
+The reference's `mpsim.bench` (bench.py:30-276) *simulates* Put/OMB bandwidth,
+bidirectional bandwidth and latency with a lifecycle breakdown, and reports
+rows `benchmark,topology,size,window,gpu_paths,host,graph_mode,chunks,
+metric,value,speedup` (bench.py:33, :55-97).  This module runs the same
+harnesses on the GPU through the engine and emits the same rows, so
+reference-style analysis and plots consume real B200 data:
+
+* `run_bw`      — `window` back-to-back messages per iteration; bandwidth
+                  and speedup over BASELINE_CONFIG (single direct path,
+                  per-call submission, one chunk; bench.py:30-31) measured
+                  the same way; plus the first (cache-miss) iteration;
+* `run_bibw`    — two opposite flows per window slot as one program
+                  (`Engine.send_many`), aggregate bandwidth;
+* `run_latency` — single-message latency first / steady and the four
+                  lifecycle phases measured by the engine (graph.py:24).
+Times are seconds, bandwidths bytes/s, as in the reference.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+
+from .paths import PathConfig
+
+CSV_HEADER = "benchmark,topology,size,window,gpu_paths,host,graph_mode,chunks,metric,value,speedup"
+BASELINE_CONFIG = PathConfig(num_gpu_paths=1, host_path_enabled=False, max_chunks=1,
+                             graph_mode=False)
+PHASES = ("creation", "construction", "instantiation", "launch")
+
+
+@dataclass
+class BenchmarkSpec:
+    kind: str
+    sizes: list[int]
+    window: int = 1
+    iterations: int = 5
+    warmup: int = 1
+    config: PathConfig = field(default_factory=PathConfig)
+    topology: str = "b200"
+
+    def __post_init__(self):
+        if self.iterations < 1:
+            raise ValueError("iterations must be >= 1")
+        if not self.sizes:
+            raise ValueError("size list is empty")
+        if self.window < 1:
+            raise ValueError("window must be >= 1")
+
+
+@dataclass
+class BenchRow:
+    benchmark: str
+    topology: str
+    size: int
+    window: int
+    gpu_paths: int
+    host: bool
+    graph_mode: bool
+    chunks: int
+    metric: str
+    value: float
+    speedup: float | None = None
+
+    def to_csv(self) -> str:
+        speedup = "" if self.speedup is None else repr(self.speedup)
+        return (f"{self.benchmark},{self.topology},{self.size},{self.window},"
+                f"{self.gpu_paths},{'on' if self.host else 'off'},"
+                f"{'on' if self.graph_mode else 'off'},{self.chunks},"
+                f"{self.metric},{self.value!r},{speedup}")
+
+
+@dataclass
+class BenchResult:
+    rows: list[BenchRow]
+
+    def to_csv(self) -> str:
+        return "\n".join([CSV_HEADER] + [r.to_csv() for r in self.rows]) + "\n"
+
+    def value(self, size: int, metric: str) -> float:
+        for row in self.rows:
+            if row.size == size and row.metric == metric:
+                return row.value
+        raise KeyError(f"no row for size={size} metric={metric}")
+
+
+def _row(spec, config, size, metric, value, speedup=None) -> BenchRow:
+    return BenchRow(spec.kind, spec.topology, size, spec.window, config.num_gpu_paths,
+                    config.host_path_enabled, config.graph_mode, config.max_chunks, metric,
+                    float(value), speedup)
+
+
+def _buffers(engine, size, n=1):
+    import torch
+    dev = engine.device_map[0]
+    bufs = []
+    for _ in range(n):
+        src = torch.randint(0, 256, (size,), dtype=torch.uint8, device=f"cuda:{dev}")
+        bufs.append((src, torch.empty_like(src)))
+    return bufs
+
+
+def _iteration(engine, posts, stream):
+    """Device seconds of one iteration: `posts` is a list of callables."""
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for post in posts:
+        post()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / 1e3
+
+
+def _measure(engine, spec, posts, stream):
+    first = _iteration(engine, posts, stream)  # pays the cache miss in graph mode
+    for _ in range(max(0, spec.warmup - 1)):
+        _iteration(engine, posts, stream)
+    times = [_iteration(engine, posts, stream) for _ in range(spec.iterations)]
+    return first, sum(times) / len(times)
+
+
+def run_bw(spec: BenchmarkSpec, engine, src_dev: int = 0, dst_dev: int = 1) -> BenchResult:
+    """Unidirectional bandwidth with a posting window (bench.py:185-210), measured."""
+    import torch
+    rows = []
+    stream = torch.cuda.Stream(device=engine.device_map[src_dev])
+    for size in spec.sizes:
+        (src, dst), = _buffers(engine, size)
+
+        def sweep(cfg):
+            engine.clear_cache()
+            post = lambda: engine.send(src, dst, size, cfg, stream=stream,  # noqa: E731
+                                       src_dev=src_dev, dst_dev=dst_dev)
+            return _measure(engine, spec, [post] * spec.window, stream)
+        first, mean = sweep(spec.config)
+        base_first, base_mean = sweep(BASELINE_CONFIG)
+        bw, base_bw = spec.window * size / mean, spec.window * size / base_mean
+        rows.append(_row(spec, spec.config, size, "bandwidth", bw, bw / base_bw))
+        rows.append(_row(spec, spec.config, size, "first_iteration_makespan", first))
+    return BenchResult(rows)
+
+
+def run_bibw(spec: BenchmarkSpec, engine, a: int = 0, b: int = 1) -> BenchResult:
+    """Bidirectional bandwidth (bench.py:213-235): flows a->b and b->a posted
+    together as one program per window slot; aggregate reported."""
+    import torch
+    rows = []
+    stream = torch.cuda.Stream(device=engine.device_map[a])
+    for size in spec.sizes:
+        (s1, d1), (s2, d2) = _buffers(engine, size, 2)
+
+        def aggregate(cfg):
+            engine.clear_cache()
+            post = lambda: engine.send_many([(s1, d1, size, a, b), (s2, d2, size, b, a)],  # noqa
+                                            cfg, stream=stream)
+            _, mean = _measure(engine, spec, [post] * spec.window, stream)
+            return 2 * spec.window * size / mean
+        bw = aggregate(spec.config)
+        base = aggregate(BASELINE_CONFIG)
+        rows.append(_row(spec, spec.config, size, "bandwidth", bw, bw / base))
+    return BenchResult(rows)
+
+
+def run_latency(spec: BenchmarkSpec, engine, src_dev: int = 0, dst_dev: int = 1) -> BenchResult:
+    """Single-message latency and the measured lifecycle phases (bench.py:238-276)."""
+    import torch
+    rows = []
+    stream = torch.cuda.Stream(device=engine.device_map[src_dev])
+    for size in spec.sizes:
+        (src, dst), = _buffers(engine, size)
+        cfgs = {"cfg": spec.config, "base": BASELINE_CONFIG}
+        res = {}
+        for name, cfg in cfgs.items():
+            engine.clear_cache()
+            post = lambda c=cfg: engine.send(src, dst, size, c, stream=stream,  # noqa: E731
+                                             src_dev=src_dev, dst_dev=dst_dev)
+            first = _iteration(engine, [post], stream)
+            first_stats = engine.stats()
+            for _ in range(3):
+                _iteration(engine, [post], stream)
+            steady = min(_iteration(engine, [post], stream) for _ in range(spec.iterations))
+            res[name] = (first, steady, first_stats, engine.stats())
+        first, steady, fst, sst = res["cfg"]
+        rows.append(_row(spec, spec.config, size, "nodes", fst.nodes_logical))
+        rows.append(_row(spec, spec.config, size, "latency_first", first, res["base"][0] / first))
+        rows.append(_row(spec, spec.config, size, "latency_steady", steady,
+                         res["base"][1] / steady))
+        if spec.config.graph_mode:
+            for phase in PHASES:
+                c_first = getattr(fst, f"{phase}_us") * 1e-6
+                c_steady = (sst.launch_us if phase == "launch" else 0.0) * 1e-6
+                rows.append(_row(spec, spec.config, size, f"phase_{phase}_first", c_first))
+                rows.append(_row(spec, spec.config, size, f"fraction_{phase}_first",
+                                 c_first / first))
+                rows.append(_row(spec, spec.config, size, f"phase_{phase}_steady", c_steady))
+                rows.append(_row(spec, spec.config, size, f"fraction_{phase}_steady",
+                                 c_steady / steady))
+        else:
+            sub = sst.launch_us * 1e-6
+            rows.append(_row(spec, spec.config, size, "phase_submission_first", sub))
+            rows.append(_row(spec, spec.config, size, "fraction_submission_first", sub / first))
+    return BenchResult(rows)
+
+
+def with_chunks(config: PathConfig, chunks: int) -> PathConfig:
+    return replace(config, max_chunks=chunks)

@@ -1,0 +1,32 @@
+"""Measured harness in the reference's CSV schema (bench.py:33): rows parse
+with the reference's own column layout and carry real, positive values."""
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def test_bw_bibw_latency_rows():
+    from paper_2604_22228_b200 import Engine, PathConfig
+    from paper_2604_22228_b200 import measure as M
+    eng = Engine.loopback(2)
+    cfg = PathConfig(num_gpu_paths=1, host_path_enabled=True, max_chunks=4, graph_mode=True)
+    sizes = [1 << 20, 8 << 20]
+    bw = M.run_bw(M.BenchmarkSpec("omb_bw", sizes, window=4, iterations=3, config=cfg), eng)
+    bibw = M.run_bibw(M.BenchmarkSpec("omb_bibw", sizes, window=2, iterations=2, config=cfg), eng)
+    lat = M.run_latency(M.BenchmarkSpec("omb_latency", sizes, iterations=3, config=cfg), eng)
+    for res in (bw, bibw, lat):
+        lines = res.to_csv().splitlines()
+        assert lines[0] == M.CSV_HEADER
+        for line in lines[1:]:
+            f = line.split(",")
+            assert len(f) == 11 and float(f[9]) >= 0.0
+    assert bw.value(8 << 20, "bandwidth") > 1e9
+    assert bibw.value(8 << 20, "bandwidth") > 1e9
+    assert lat.value(1 << 20, "phase_instantiation_first") > 0.0
+    import paper_2604_22228_b200 as mp
+    topo = eng.topology
+    plan = mp.make_chunk_plan(mp.plan_paths(topo, topo.device(0), topo.device(1), cfg), 1 << 20, 4)
+    assert lat.value(1 << 20, "nodes") == mp.build_graph(plan).node_count
+    eng.close()
