@@ -402,6 +402,8 @@ def run_ours(args, rank, world):
 
     # 6. lifecycle (BASELINE config 5) and the reference's CPU path
     lifecycle = None if args.quick else run_lifecycle(torch, eng, dev, stream)
+    relays = None if args.quick else run_relay_sweep(torch, dev, size, link_bw, host_bw,
+                                                     hbm_peak / 2, pcie)
     cpu, ref_cpu = None, None
     if rank == 0 and not args.quick:
         cpu_rate, nmsg = cpu_transfer_rate(size, args.chunks, 10.0, len(os.sched_getaffinity(0)))
@@ -440,6 +442,7 @@ def run_ours(args, rank, world):
                   "kernels_per_send": st.kernels, "ce_copies_per_send": st.ce_copies,
                   "launch_us": st.launch_us},
         "lifecycle": lifecycle,
+        "relay_sweep": relays,
         "sweep": sweep,
         "tuning_csv": tuning,
     }
@@ -489,6 +492,34 @@ def run_sweep(torch, eng, topo_text, dev, stream):
     return rows, {"table_csv": table.to_csv(), "engine_policy": rules}
 
 
+def run_relay_sweep(torch, dev, size, link_bw, host_bw, hbm_copy, pcie):
+    """BASELINE config 4 in loopback: 8 logical GPUs on one B200, direct +
+    0..6 GPU relays + host, max_chunks 16.  Every relayed byte is copied twice
+    through the same HBM, so the gain the reference's model predicts (an
+    independent channel per pair, topology.py:112-120) cannot appear: this is
+    the single-GPU image of the NVSwitch ingress/egress cap."""
+    from paper_2604_22228_b200 import Engine, PathConfig, load_topology, mesh_text
+    eng8 = Engine(load_topology(mesh_text("b200x8_loopback", 8, link_bw, 1, 2e-6, host_bw, 1e-5,
+                                          "full")), [dev] * 8)
+    src = torch.empty(size, dtype=torch.uint8, device=f"cuda:{dev}")
+    dst = torch.empty_like(src)
+    stream = torch.cuda.Stream(device=dev)
+    rows = []
+    for g in range(1, 8):
+        cfg = PathConfig(num_gpu_paths=g, host_path_enabled=True, max_chunks=16, graph_mode=True)
+        t = time_sends(torch, eng8, cfg, src, dst, size, 10, 3, stream)
+        st = eng8.stats()
+        relay_share = sum(p.share for p in eng8.last_plan()[0] if p.kind == "gpu")
+        # loopback roofline: a relayed byte costs two HBM copies
+        r = 1.0 / ((1 - relay_share) / hbm_copy + 2 * relay_share / hbm_copy) + pcie
+        rows.append({"relays": g - 1, "gbs": size / t / 1e9, "relay_share": relay_share,
+                     "loopback_roofline_gbs": r, "frac": size / t / 1e9 / r,
+                     "nodes_logical": st.nodes_logical, "nodes_physical": st.nodes_physical,
+                     "kernels": st.kernels})
+    eng8.close()
+    return rows
+
+
 def run_lifecycle(torch, eng, dev, stream):
     """Capture+instantiate every call / cached replay / per-call stream launch:
     host us per message, GPU latency, and the four lifecycle phases."""
@@ -516,7 +547,7 @@ def run_lifecycle(torch, eng, dev, stream):
             for _ in range(10):
                 eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
             torch.cuda.synchronize()
-            n = 2000
+            n = 10000  # BASELINE config 5: 10k iterations per size and arm
             t0 = time.perf_counter()
             for _ in range(n):
                 eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)

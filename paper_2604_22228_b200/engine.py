@@ -189,6 +189,12 @@ class Engine:
             if not cands:
                 raise ValueError("cannot infer the logical destination device; pass dst_dev")
             dst_dev = cands[0]
+        if (src.device.index, dst.device.index) != (self.device_map[src_dev],
+                                                    self.device_map[dst_dev]):
+            raise ValueError(f"src/dst tensors live on cuda:{src.device.index}/"
+                             f"cuda:{dst.device.index}, but logical devices {src_dev}/{dst_dev} "
+                             f"map to cuda:{self.device_map[src_dev]}/"
+                             f"cuda:{self.device_map[dst_dev]}")
         if stream is None:
             stream = torch.cuda.current_stream(src.device)
         handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
