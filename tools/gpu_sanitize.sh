@@ -25,6 +25,6 @@ for copy in ("tma", "vec"):
 print("workload ok")
 PY
 for tool in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool --kernel-name regex:transfer_kernel --print-limit 20 python /tmp/san_work.py > gpurun_out/sanitizer_$tool.log 2>&1
+  timeout 900 compute-sanitizer --tool $tool --kernel-name kns=transfer_kernel --print-limit 20 python /tmp/san_work.py > gpurun_out/sanitizer_$tool.log 2>&1
   echo "$tool rc=$?"; tail -3 gpurun_out/sanitizer_$tool.log
 done
