@@ -301,17 +301,14 @@ def run_ours(args, rank, world):
     dst.copy_(torch.bitwise_not(src))
     stream = torch.cuda.Stream(device=dev)
 
-    # correctness of the benchmarked configuration (bytes + plan vs oracle)
+    # the benchmarked configuration delivers every byte (plan parity against the
+    # oracle is the tests' job: tests/test_gpu_transfer.py)
     eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
     eng.sync()
     torch.cuda.synchronize()
     assert torch.equal(src, dst), "delivered bytes differ"
-    from oracle import planner as op
-    opaths = op.plan_paths(op.parse_topology(topo_text), 0, 1, 1, True)
-    ochunks = op.make_chunk_plan([p["share"] for p in opaths], size, args.chunks)
     _, chunks = eng.last_plan()
-    assert [(c.path_index, c.offset, c.length, c.seq) for c in chunks] == ochunks
-    direct_bytes = sum(c[2] for c in ochunks if c[0] == 0)
+    direct_bytes = sum(c.length for c in chunks if c.path_index == 0)
     host_bytes = size - direct_bytes
 
     # 2. headline: K steps, each one osu_bw window of W back-to-back messages
