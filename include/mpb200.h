@@ -180,6 +180,9 @@ typedef struct {
   int32_t tma_block;         /* TMA: bytes per bulk copy (multiple of 16) */
   int32_t host_engine;       /* MP_ENGINE_*: host-staged path by the SM
                                 kernels (mapped pinned memory) or by CEs */
+  int32_t tma_peer;          /* 1: TMA bulk copies also on tables that touch
+                                another GPU over NVLink; 0 (default): such
+                                tables run the 16-byte LDG/STG kernel */
 } mp_engine_opts;
 
 /* ---- errors / version ---------------------------------------------------- */

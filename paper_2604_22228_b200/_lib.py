@@ -109,7 +109,7 @@ class mp_engine_opts(C.Structure):
                 ("copy_kind", C.c_int32), ("ctas_per_sm", C.c_int32), ("threads", C.c_int32),
                 ("tile_bytes", C.c_int64), ("host_slots", C.c_int32), ("pull", C.c_int32),
                 ("sm_min_bytes", C.c_int64), ("unroll", C.c_int32), ("tma_stages", C.c_int32),
-                ("tma_block", C.c_int32), ("host_engine", C.c_int32)]
+                ("tma_block", C.c_int32), ("host_engine", C.c_int32), ("tma_peer", C.c_int32)]
 
 
 P = C.POINTER

@@ -29,6 +29,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -66,9 +67,19 @@ size_t kernel_smem(const mp_engine_opts& o) {
 // Launch the persistent transfer kernel (mp_kernels.cuh) over one tile table.
 // `nstatic` > 0 only for tables without flag waits: static first tiles must
 // never be waited on by another CTA (residency of every CTA is not guaranteed).
-void launch_transfer(const mp_engine_opts& o, unsigned grid, cudaStream_t s, const mpk::Tile* tiles,
+void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, const mpk::Tile* tiles,
                      unsigned ntiles, mpk::Ctl* ctl, unsigned nstatic,
-                     unsigned long long* trace = nullptr, const mpk::GroupSync* gsync = nullptr) {
+                     unsigned long long* trace = nullptr, const mpk::GroupSync* gsync = nullptr,
+                     bool peer = false, int sms = 148) {
+  mp_engine_opts o = o_in;
+  if (peer && !o.tma_peer && o.copy_kind == MP_COPY_TMA) {
+    // NVLink peer tables: the 16-byte LDG/STG kernel (2 x 256 threads per SM)
+    o.copy_kind = MP_COPY_VEC;
+    o.unroll = 8;
+    o.threads = 256;
+    grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sms * 2);
+    nstatic = nstatic ? grid : 0;
+  }
   KernelFn fn = pick_kernel(o);
   size_t smem = kernel_smem(o);
   if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -131,6 +142,7 @@ struct Program {
   unsigned ntiles = 0;
   unsigned grid = 0;
   unsigned nstatic = 0;  // = grid when the table has no flag waits
+  bool peer = false;     // some tile reads or writes another GPU's memory
 };
 
 struct Entry {
@@ -430,6 +442,7 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
   ensure_arenas(ctx, stage_need, flag_devs, total_chunks, host_need);
 
   std::vector<std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>> tiles(ctx->phys.size());
+  std::vector<char> peer_phys(ctx->phys.size(), 0);
   std::vector<uint64_t> stage_cursor(ctx->logi.size(), 0);  // shared relay arenas
   uint64_t host_cursor = 0;                                  // shared pinned arena
   auto new_event = [&](int phys) {
@@ -444,6 +457,14 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
     const int np = (int)paths.size(), nc = (int)chunks[t].size();
     const int sp = ctx->logi[x.sd].phys, dp = ctx->logi[x.dd].phys;
     const uint64_t s0 = (uint64_t)(uintptr_t)x.src, d0 = (uint64_t)(uintptr_t)x.dst;
+    // tables that touch another GPU's memory over NVLink (see launch_transfer)
+    if (sp != dp) peer_phys[o.pull ? dp : sp] = 1;
+    for (const mp_path& P : paths)
+      if (P.kind == MP_PATH_GPU) {
+        const int rp = ctx->logi[P.stage].phys;
+        if (rp != sp) peer_phys[sp] = 1;
+        if (rp != dp) peer_phys[rp] = 1;
+      }
     std::vector<int> lane_base(np, 0);
     for (int p = 0; p < np; ++p) {
       lane_base[p] = lane_next;
@@ -587,6 +608,7 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
     bool waits = false;
     for (const auto& tl : flat) waits |= tl.wait != nullptr;
     pr.nstatic = waits ? 0u : pr.grid;
+    pr.peer = peer_phys[ph] != 0;
     CK(cudaSetDevice(P.ordinal));
     CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile)));
     e->progs.push_back(pr);  // owned by the entry from here (freed on error)
@@ -634,7 +656,8 @@ void enqueue_group(mp_ctx* ctx, Entry* e, cudaStream_t origin) {
   mpk::GroupSync g = group_sync(ctx);
   if (!e->progs.empty()) {
     const Program& pr = e->progs[0];
-    launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic, nullptr, &g);
+    launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic, nullptr, &g,
+                    pr.peer, P.sms);
   } else if (e->grole == 3) {
     mpk::group_recv_kernel<<<1, 32, 0, P.kstream>>>(g, ctx->group->done(ctx->group->rank), e->expected,
                                                     P.ctl);
@@ -685,7 +708,7 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr 
     if (t) ctx->timed_phys = pr.phys;
     if (t) CK(cudaEventRecord(P.kt0, P.kstream));
     launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic,
-                    tr ? tr->stamps[pr.phys] : nullptr);
+                    tr ? tr->stamps[pr.phys] : nullptr, nullptr, pr.peer, P.sms);
     if (t) CK(cudaEventRecord(P.kt1, P.kstream));
   }
   // copy-engine lanes
@@ -894,6 +917,19 @@ Entry* build_group_entry(mp_ctx* ctx, const std::string& key, const void* src, u
     bool waits = false;
     for (const auto& t : flat) waits |= t.wait != nullptr;
     pr.nstatic = waits ? 0u : pr.grid;
+    // IPC-mapped buffers of another physical GPU make this an NVLink table
+    const int here = ctx->phys[0].ordinal;
+    std::set<uint64_t> seen;  // one query per 16 MiB region
+    for (const auto& t : flat)
+      for (uint64_t a : {t.src, t.dst}) {
+        if (!seen.insert(a >> 24).second) continue;
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, (const void*)(uintptr_t)a) == cudaSuccess &&
+            at.type == cudaMemoryTypeDevice && at.device != here)
+          pr.peer = true;
+        else
+          cudaGetLastError();
+      }
     CK(cudaSetDevice(ctx->phys[0].ordinal));
     CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile)));
     CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
@@ -1427,10 +1463,12 @@ int mp_kernel_bench(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int3
   Phys& S = ctx->phys[e->src_phys];
   CK(cudaSetDevice(S.ordinal));
   CK(cudaDeviceSynchronize());
-  launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic);  // warm
+  launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
+                  nullptr, pr->peer, S.sms);  // warm
   CK(cudaEventRecord(S.kt0, S.kstream));
   for (int i = 0; i < reps; ++i)
-    launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic);
+    launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
+                    nullptr, pr->peer, S.sms);
   CK(cudaEventRecord(S.kt1, S.kstream));
   CK(cudaEventSynchronize(S.kt1));
   float ms = 0.f;

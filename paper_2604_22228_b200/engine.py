@@ -107,10 +107,13 @@ class Engine:
                   tile_bytes: int | None = None, host_slots: int | None = None,
                   pull: bool | None = None, sm_min_bytes: int | None = None,
                   copy: str | None = None, unroll: int | None = None,
-                  tma_stages: int | None = None, tma_block: int | None = None) -> None:
+                  tma_stages: int | None = None, tma_block: int | None = None,
+                  tma_peer: bool | None = None) -> None:
         """Pick the copy mechanism per path type and the SM-kernel shape."""
         o = _lib.mp_engine_opts()
         check(lib.mp_ctx_get_engine(self._ctx, C.byref(o)))
+        if tma_peer is not None:
+            o.tma_peer = int(tma_peer)
         if copy is not None:
             o.copy_kind = COPIES[copy]
         if unroll is not None:
