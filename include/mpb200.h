@@ -182,7 +182,8 @@ typedef struct {
                                 kernels (mapped pinned memory) or by CEs */
   int32_t tma_peer;          /* 1: TMA bulk copies also on tables that touch
                                 another GPU over NVLink; 0 (default): such
-                                tables run the 16-byte LDG/STG kernel */
+                                tables run the 16-byte LDG/STG kernel;
+                                -1: every table does (testing)        */
 } mp_engine_opts;
 
 /* ---- errors / version ---------------------------------------------------- */

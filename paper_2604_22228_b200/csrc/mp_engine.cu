@@ -72,7 +72,8 @@ void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, 
                      unsigned long long* trace = nullptr, const mpk::GroupSync* gsync = nullptr,
                      bool peer = false, int sms = 148) {
   mp_engine_opts o = o_in;
-  if (peer && !o.tma_peer && o.copy_kind == MP_COPY_TMA) {
+  if ((o.tma_peer < 0 || (peer && o.tma_peer == 0)) && o.copy_kind == MP_COPY_TMA) {
+    // (tma_peer < 0 forces this path on every table: single-GPU testing)
     // NVLink peer tables: the 16-byte LDG/STG kernel (2 x 256 threads per SM)
     o.copy_kind = MP_COPY_VEC;
     o.unroll = 8;

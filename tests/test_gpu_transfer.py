@@ -205,3 +205,13 @@ def test_probe_node_writes_a_plannable_topology():
                        mp.PathConfig(num_gpu_paths=2, host_path_enabled=True))
     assert abs(sum(p.share for p in ps.paths) - 1.0) < 1e-12
     eng.close()
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_peer_table_fallback_kernel(graph):
+    """Tables touching another GPU run the LDG/STG kernel (tma_peer = 0);
+    tma_peer = -1 forces that launch path on one GPU so it is exercised."""
+    eng, text = _engine(4, tma_peer=-1)
+    _check(eng, text, 8 * MiB + 333, gpu_paths=3, host=True, chunks=4, graph=graph,
+           policy="equal", src_off=3, dst_off=3, reps=2, seed=9)
+    eng.close()
