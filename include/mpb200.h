@@ -164,6 +164,10 @@ typedef struct {
 #define MP_ENGINE_CE 1       /* copy engine cudaMemcpyAsync            */
 #define MP_COPY_VEC 0        /* 16-byte vector LDG/STG                 */
 #define MP_COPY_TMA 1        /* cp.async.bulk staged through smem      */
+#define MP_SCHED_AUTO 0      /* static one-tile-per-CTA tables where no
+                                tile waits or touches host memory (no
+                                atomics, no exit protocol); else dynamic */
+#define MP_SCHED_DYNAMIC 1   /* always claim tiles dynamically          */
 
 typedef struct {
   int32_t direct_engine;     /* MP_ENGINE_*                           */
@@ -184,6 +188,9 @@ typedef struct {
                                 another GPU over NVLink; 0 (default): such
                                 tables run the 16-byte LDG/STG kernel;
                                 -1: every table does (testing)        */
+  int32_t sched;             /* MP_SCHED_*: tile scheduling of the SM kernel */
+  int64_t small_max_bytes;   /* static direct tables up to this size run the
+                                one-launch-slot small-message kernel (0 = off) */
 } mp_engine_opts;
 
 /* ---- errors / version ---------------------------------------------------- */

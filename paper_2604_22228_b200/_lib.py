@@ -32,6 +32,7 @@ MP_SHARE_BANDWIDTH, MP_SHARE_EQUAL = 0, 1
 MP_DUPLEX_FULL, MP_DUPLEX_HALF = 0, 1
 MP_ENGINE_SM, MP_ENGINE_CE = 0, 1
 MP_COPY_VEC, MP_COPY_TMA = 0, 1
+MP_SCHED_AUTO, MP_SCHED_DYNAMIC = 0, 1
 
 
 class mp_config(C.Structure):
@@ -109,7 +110,8 @@ class mp_engine_opts(C.Structure):
                 ("copy_kind", C.c_int32), ("ctas_per_sm", C.c_int32), ("threads", C.c_int32),
                 ("tile_bytes", C.c_int64), ("host_slots", C.c_int32), ("pull", C.c_int32),
                 ("sm_min_bytes", C.c_int64), ("unroll", C.c_int32), ("tma_stages", C.c_int32),
-                ("tma_block", C.c_int32), ("host_engine", C.c_int32), ("tma_peer", C.c_int32)]
+                ("tma_block", C.c_int32), ("host_engine", C.c_int32), ("tma_peer", C.c_int32),
+                ("sched", C.c_int32), ("small_max_bytes", C.c_int64)]
 
 
 P = C.POINTER

@@ -70,7 +70,12 @@ size_t kernel_smem(const mp_engine_opts& o) {
 void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, const mpk::Tile* tiles,
                      unsigned ntiles, mpk::Ctl* ctl, unsigned nstatic,
                      unsigned long long* trace = nullptr, const mpk::GroupSync* gsync = nullptr,
-                     bool peer = false, int sms = 148) {
+                     bool peer = false, int sms = 148, const mpk::SmallTable* small = nullptr) {
+  if (small && !trace && !gsync) {  // small static direct table: one-slot kernel
+    mpk::small_copy_kernel<4><<<ntiles, 256, 0, s>>>(*small);
+    CK(cudaGetLastError());
+    return;
+  }
   mp_engine_opts o = o_in;
   if ((o.tma_peer < 0 || (peer && o.tma_peer == 0)) && o.copy_kind == MP_COPY_TMA) {
     // (tma_peer < 0 forces this path on every table: single-GPU testing)
@@ -144,6 +149,7 @@ struct Program {
   unsigned grid = 0;
   unsigned nstatic = 0;  // = grid when the table has no flag waits
   bool peer = false;     // some tile reads or writes another GPU's memory
+  std::shared_ptr<mpk::SmallTable> small;  // small static direct table (kernel params)
 };
 
 struct Entry {
@@ -296,6 +302,19 @@ void ensure_arenas(mp_ctx* ctx, const std::vector<size_t>& stage_need,
 // Host-path tiles stay small so many CTAs keep PCIe requests in flight.
 constexpr uint64_t kHostTileBytes = 64 << 10;
 
+// Smallest tile of a static (one-tile-per-CTA) table: below this a message
+// spreads over fewer CTAs rather than into sub-4 KiB slivers.
+constexpr uint64_t kStaticMinTile = 4096;
+// Largest per-CTA share of a static table.  Measured crossover (loopback,
+// tools/abi_latency.cu): static wins up to 64 MiB (16 MiB: 6.2 vs 10.2 us per
+// message), dynamic claims win from 128 MiB (512 MiB: 166.8 vs 178.2 us) —
+// per-SM copy rates are not uniform enough for one fixed share per CTA.
+constexpr uint64_t kStaticMaxPerCta = 640 << 10;
+// Default ceiling of the small-message kernel (engine opts small_max_bytes):
+// measured 1 launch slot up to 64 KiB, 3.0 us at 1 MiB (TMA kernel 4.1),
+// a tie at 4 MiB, and 8.2 vs 6.2 us at 16 MiB (tools/abi_latency.cu).
+constexpr int64_t kSmallMaxBytes = 4 << 20;
+
 uint64_t auto_tile_bytes(const mp_ctx* ctx, uint64_t path_bytes, int sms) {
   if (ctx->opts.tile_bytes > 0) return (uint64_t)ctx->opts.tile_bytes;
   // aim for >= 12 tiles per resident CTA (the tail is at most one tile),
@@ -442,6 +461,50 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
   }
   ensure_arenas(ctx, stage_need, flag_devs, total_chunks, host_need);
 
+  // Static schedule (MP_SCHED_AUTO): a device whose tiles never wait on a flag
+  // and never touch host memory, and whose share is <= kStaticMaxPerCta per
+  // CTA, gets ONE tile per CTA — tile bytes = its SM
+  // bytes over (grid - 2 x segments), so cutting every chunk-hop segment
+  // still yields <= grid tiles.  The kernel then runs with no claim atomics
+  // and no exit protocol (mp_kernels.cuh); every CTA streams an equal share.
+  // Devices with waits or PCIe tiles keep dynamic claims (load balance).
+  std::vector<uint64_t> static_tile(ctx->phys.size(), 0);
+  if (o.sched == MP_SCHED_AUTO && o.tile_bytes == 0) {
+    const size_t nph = ctx->phys.size();
+    std::vector<uint64_t> sm_bytes(nph, 0);
+    std::vector<int> segs(nph, 0);
+    std::vector<char> dyn(nph, 0);
+    for (int t = 0; t < T; ++t) {
+      const int sp = ctx->logi[xs[t].sd].phys, dp = ctx->logi[xs[t].dd].phys;
+      for (const mp_chunk& c : chunks[t]) {
+        const mp_path& P = xs[t].paths[c.path_index];
+        if (P.kind == MP_PATH_DIRECT && eng[t].direct_sm) {
+          const int ex = o.pull ? dp : sp;
+          sm_bytes[ex] += c.length;
+          segs[ex] += 1;
+        } else if (P.kind == MP_PATH_GPU && eng[t].relay_sm) {
+          sm_bytes[sp] += c.length;
+          segs[sp] += 1;
+          dyn[ctx->logi[P.stage].phys] = 1;
+        } else if (P.kind == MP_PATH_HOST && eng[t].host_sm) {
+          dyn[sp] = dyn[dp] = 1;
+        }
+      }
+    }
+    for (size_t ph = 0; ph < nph; ++ph) {
+      const uint64_t grid = (uint64_t)ctx->phys[ph].sms * std::max(1, o.ctas_per_sm);
+      if (dyn[ph] || segs[ph] == 0 || (uint64_t)segs[ph] * 4 > grid ||
+          sm_bytes[ph] > grid * kStaticMaxPerCta)
+        continue;
+      uint64_t tb = (sm_bytes[ph] + (grid - 2 * segs[ph]) - 1) / (grid - 2 * segs[ph]);
+      tb = std::max<uint64_t>(tb, kStaticMinTile);
+      static_tile[ph] = (tb + 15) & ~(uint64_t)15;
+    }
+  }
+  auto tile_for = [&](int ph, uint64_t path_bytes) {
+    return static_tile[ph] ? static_tile[ph] : auto_tile_bytes(ctx, path_bytes, ctx->phys[ph].sms);
+  };
+
   std::vector<std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>> tiles(ctx->phys.size());
   std::vector<char> peer_phys(ctx->phys.size(), 0);
   std::vector<uint64_t> stage_cursor(ctx->logi.size(), 0);  // shared relay arenas
@@ -494,7 +557,7 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
           mpk::Tile proto{};
           proto.node = n_a;
           append_tiles(tiles[exec], order(r2), s0 + ch.offset, d0 + ch.offset, ch.length,
-                       auto_tile_bytes(ctx, pi.bytes, ctx->phys[exec].sms), proto);
+                       tile_for(exec, pi.bytes), proto);
         } else {
           e->ce.push_back(CeOp{sp, lane_base[p], (uint8_t*)x.dst + ch.offset,
                                (const uint8_t*)x.src + ch.offset, (size_t)ch.length, -1, -1, n_a});
@@ -508,7 +571,7 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
         uint8_t* stage = L.stage + cur;
         cur += ch.length;
         if (eng[t].relay_sm) {
-          uint64_t t1 = auto_tile_bytes(ctx, pi.bytes, ctx->phys[sp].sms);
+          uint64_t t1 = tile_for(sp, pi.bytes);
           uint64_t t2 = auto_tile_bytes(ctx, pi.bytes, ctx->phys[rp].sms);
           mpk::Tile h1{};
           h1.signal = L.flags + g;
@@ -614,6 +677,22 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
     CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile)));
     e->progs.push_back(pr);  // owned by the entry from here (freed on error)
     CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
+    // small static table of plain direct tiles: the one-slot small kernel
+    uint64_t tbytes = 0;
+    bool plain = flat.size() <= mpk::kSmallMaxTiles;
+    for (const auto& tl : flat) {
+      tbytes += tl.len;
+      plain = plain && !tl.wait && !tl.signal && tl.flags == 0;
+    }
+    if (plain && o.sched == MP_SCHED_AUTO && tbytes <= (uint64_t)o.small_max_bytes) {
+      auto sm = std::make_shared<mpk::SmallTable>();
+      for (size_t i = 0; i < flat.size(); ++i) {
+        sm->src[i] = flat[i].src;
+        sm->dst[i] = flat[i].dst;
+        sm->len[i] = (uint32_t)flat[i].len;
+      }
+      e->progs.back().small = sm;
+    }
   }
   return e.release();
 }
@@ -658,7 +737,7 @@ void enqueue_group(mp_ctx* ctx, Entry* e, cudaStream_t origin) {
   if (!e->progs.empty()) {
     const Program& pr = e->progs[0];
     launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic, nullptr, &g,
-                    pr.peer, P.sms);
+                    pr.peer, P.sms, pr.small.get());
   } else if (e->grole == 3) {
     mpk::group_recv_kernel<<<1, 32, 0, P.kstream>>>(g, ctx->group->done(ctx->group->rank), e->expected,
                                                     P.ctl);
@@ -709,7 +788,7 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr 
     if (t) ctx->timed_phys = pr.phys;
     if (t) CK(cudaEventRecord(P.kt0, P.kstream));
     launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic,
-                    tr ? tr->stamps[pr.phys] : nullptr, nullptr, pr.peer, P.sms);
+                    tr ? tr->stamps[pr.phys] : nullptr, nullptr, pr.peer, P.sms, pr.small.get());
     if (t) CK(cudaEventRecord(P.kt1, P.kstream));
   }
   // copy-engine lanes
@@ -1000,6 +1079,8 @@ int mp_ctx_create(int32_t n_logical, const int32_t* device_map, mp_ctx** out) {
   ctx->opts.unroll = 8;
   ctx->opts.tma_stages = 4;
   ctx->opts.tma_block = 32768;
+  ctx->opts.sched = MP_SCHED_AUTO;
+  ctx->opts.small_max_bytes = kSmallMaxBytes;
   std::map<int, int> phys_of;
   for (int i = 0; i < n_logical; ++i) {
     int ord = device_map[i];
@@ -1122,6 +1203,9 @@ int mp_ctx_set_engine(mp_ctx* ctx, const mp_engine_opts* o) {
   if (o->direct_engine < 0 || o->direct_engine > 1 || o->relay_engine < 0 || o->relay_engine > 1 ||
       o->host_engine < 0 || o->host_engine > 1)
     return fail(MP_ERR_VALUE, "unknown engine");
+  if (o->sched != MP_SCHED_AUTO && o->sched != MP_SCHED_DYNAMIC) return fail(MP_ERR_VALUE, "unknown sched");
+  if (o->small_max_bytes < 0 || o->small_max_bytes > (int64_t)1 << 31)
+    return fail(MP_ERR_VALUE, "small_max_bytes must be in [0, 2^31]");
   std::lock_guard<std::mutex> lk(ctx->mu);
   clear_cache(ctx);
   ctx->opts = *o;
@@ -1465,11 +1549,11 @@ int mp_kernel_bench(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int3
   CK(cudaSetDevice(S.ordinal));
   CK(cudaDeviceSynchronize());
   launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
-                  nullptr, pr->peer, S.sms);  // warm
+                  nullptr, pr->peer, S.sms, pr->small.get());  // warm
   CK(cudaEventRecord(S.kt0, S.kstream));
   for (int i = 0; i < reps; ++i)
     launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
-                    nullptr, pr->peer, S.sms);
+                    nullptr, pr->peer, S.sms, pr->small.get());
   CK(cudaEventRecord(S.kt1, S.kstream));
   CK(cudaEventSynchronize(S.kt1));
   float ms = 0.f;

@@ -351,7 +351,9 @@ struct TmaEngine {
   Tile ahead;
   unsigned claim2;
   unsigned nstatic;  // tiles [0, nstatic) go to CTA blockIdx.x without a claim
-  __device__ unsigned claim() { return atomicAdd(&ctl->work, 1u) + nstatic; }
+  __device__ unsigned claim() {
+    return nstatic >= ntiles ? ntiles : atomicAdd(&ctl->work, 1u) + nstatic;
+  }
   __device__ void prime() {
     next_claim = blockIdx.x < nstatic ? blockIdx.x : claim();
     claim2 = claim();
@@ -432,6 +434,56 @@ struct TmaEngine {
   }
 };
 
+// ---------------------------------------------------------------------------
+// Small-message kernel.  Back-to-back launches on one stream complete in
+// ~2.05 us "slots" (tools/kexp.cu: an empty kernel takes one slot, a kernel
+// whose body runs >~0.7 us takes two).  A small message therefore has a
+// budget of about one L2 round trip: its descriptor comes from the kernel
+// parameters (constant bank, no dependent global load), every thread issues
+// all its 16-byte loads before any store, and there is no shared memory, no
+// barrier, no claim and no exit protocol.  Used for static tables of direct
+// tiles only (no flags, no host memory), one tile per CTA.
+// ---------------------------------------------------------------------------
+constexpr unsigned kSmallMaxTiles = 148;
+struct SmallTable {
+  uint64_t src[kSmallMaxTiles];
+  uint64_t dst[kSmallMaxTiles];
+  uint32_t len[kSmallMaxTiles];
+};
+
+template <int V>
+__global__ void __launch_bounds__(256) small_copy_kernel(const __grid_constant__ SmallTable tab) {
+  const uint8_t* src = (const uint8_t*)tab.src[blockIdx.x];
+  uint8_t* dst = (uint8_t*)tab.dst[blockIdx.x];
+  const uint32_t len = tab.len[blockIdx.x];
+  const uint32_t tid = threadIdx.x, nt = blockDim.x;
+  if ((((uintptr_t)src ^ (uintptr_t)dst) & 15u) != 0) {
+    copy_range<4, false>(src, dst, len);
+    return;
+  }
+  uint32_t head = (16u - ((uint32_t)(uintptr_t)dst & 15u)) & 15u;
+  if (head > len) head = len;
+  const uint32_t nvec = (len - head) >> 4;
+  const uint32_t tail_at = head + (nvec << 4);
+  const int4* s4 = reinterpret_cast<const int4*>(src + head);
+  int4* d4 = reinterpret_cast<int4*>(dst + head);
+  const bool hv = tid < head, tv = tid < len - tail_at;
+  uint8_t hb = 0, tb = 0;
+  if (hv) hb = src[tid];
+  if (tv) tb = src[tail_at + tid];
+  for (uint32_t base = tid; base < nvec; base += V * nt) {
+    int4 v[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (base + k * nt < nvec) v[k] = ld16_nc(s4 + base + k * nt);
+#pragma unroll
+    for (int k = 0; k < V; ++k)
+      if (base + k * nt < nvec) st16(d4 + base + k * nt, v[k]);
+  }
+  if (hv) dst[tid] = hb;
+  if (tv) dst[tail_at + tid] = tb;
+}
+
 // Time base of a traced send: %globaltimer at the fork point of this device.
 __global__ void stamp_kernel(unsigned long long* out) { *out = globaltimer(); }
 
@@ -444,6 +496,10 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
                                                        GroupSync gsync) {
   // Tiles [0, nstatic) (a prefix with no flag waits, nstatic <= gridDim.x) are
   // taken by CTA blockIdx.x without a claim; the rest are claimed dynamically.
+  // A fully static table (nstatic == ntiles: one tile per CTA, no waits) runs
+  // with no atomics and no exit protocol at all: the control block is
+  // untouched, so a small message costs one launch and one copy.
+  const bool all_static = nstatic >= ntiles && gsync.n == 0;
   __shared__ Tile s_tile;
   __shared__ int s_cmd;
   __shared__ uint64_t s_bar[16];
@@ -479,7 +535,9 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
         if (t.signal) signal_tile(t.signal, sig_bytes(t));
       }
     }
-    if (threadIdx.x == 0) bulk_wait_all();
+    // smem must outlive the last bulk store's reads; its global writes are
+    // complete at grid completion (tiles that signal waited for them above)
+    if (threadIdx.x == 0) bulk_wait_read<0>();
   } else {
     // ---- vector LDG/STG: the whole CTA copies each claimed tile ----
     __shared__ unsigned s_claim[2];
@@ -490,7 +548,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
     unsigned parity = 1;
     while (w < ntiles) {
       if (threadIdx.x == 0) {
-        s_claim[parity] = atomicAdd(&ctl->work, 1u) + nstatic;  // prefetch the next claim
+        s_claim[parity] = all_static ? ntiles : atomicAdd(&ctl->work, 1u) + nstatic;  // prefetch
         s_tile = tiles[w];
         if (s_tile.wait) wait_tile_flag(s_tile, ctl);
         trace_start(trace, s_tile.node);
@@ -511,7 +569,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       __syncthreads();  // s_tile / s_claim reuse
     }
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && !all_static) {
     __threadfence();
     if (atomicAdd(&ctl->exit, 1u) + 1u == gridDim.x) {  // last CTA re-arms the counters
       ctl->work = 0u;

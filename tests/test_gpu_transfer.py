@@ -215,3 +215,20 @@ def test_peer_table_fallback_kernel(graph):
     _check(eng, text, 8 * MiB + 333, gpu_paths=3, host=True, chunks=4, graph=graph,
            policy="equal", src_off=3, dst_off=3, reps=2, seed=9)
     eng.close()
+
+
+@pytest.mark.parametrize("mode", ["small", "static", "dynamic"])
+@pytest.mark.parametrize("size,chunks,host,offs", [
+    (1, 1, False, (0, 0)), (4095, 1, False, (3, 3)), (4096, 3, False, (0, 0)),
+    (65536 + 3, 2, True, (5, 9)), (MiB + 7, 8, False, (1, 1)), (3 * MiB + 5, 16, True, (7, 3)),
+    (20 * MiB + 1, 4, False, (0, 8)), (70 * MiB + 13, 8, True, (2, 2))])
+def test_tile_schedules(mode, size, chunks, host, offs):
+    """The three SM schedules of a direct table deliver the same bytes:
+    the one-launch-slot small kernel (static tables <= small_max_bytes), the
+    static one-tile-per-CTA TMA table, and dynamic claims — with chunked
+    (multi-segment), misaligned and direct+host (CE) plans, replayed."""
+    opts = {"small": {}, "static": {"small_max_bytes": 0}, "dynamic": {"sched": "dynamic"}}[mode]
+    eng, text = _engine(2, **opts)
+    _check(eng, text, size, host=host, chunks=chunks, graph=True, src_off=offs[0],
+           dst_off=offs[1], seed=11, reps=2)
+    eng.close()
