@@ -64,26 +64,52 @@ size_t kernel_smem(const mp_engine_opts& o) {
   return o.copy_kind == MP_COPY_TMA ? (size_t)o.tma_stages * (size_t)o.tma_block : 0;
 }
 
-// Launch the persistent transfer kernel (mp_kernels.cuh) over one tile table.
+// Kernel choice per tile table (measured, tools/abi_latency.cu, loopback):
+//  * PROG_SMALL       static table <= small_max_bytes of plain direct tiles:
+//                     small_copy_kernel, descriptors in the kernel parameters
+//                     (one ~2 us launch slot up to 64 KiB);
+//  * PROG_STATIC_TMA  static table (one tile per CTA, <= kStaticMaxPerCta):
+//                     the TMA ring kernel, 1 CTA x 128 threads per SM, no
+//                     claims and no exit protocol (16-64 MiB: 10% ahead);
+//  * PROG_DYNAMIC     everything else: the configured kernel with atomic tile
+//                     claims — by default the 16-byte LDG/STG kernel at
+//                     4 CTAs x 256 threads per SM over 64 KiB tiles, which
+//                     copies 512 MiB at 100% of the measured HBM peak (the TMA
+//                     ring, copy_kind = MP_COPY_TMA, reaches 98%).
+// Tables that touch another GPU's memory never run TMA unless tma_peer allows
+// it (TMA bulk copies on peer addresses are unverified on this 1-GPU pool).
+enum ProgKind { PROG_DYNAMIC = 0, PROG_STATIC_TMA = 1, PROG_SMALL = 2 };
+constexpr int kPeerCtasPerSm = 4;
+constexpr uint64_t kVecTileBytes = 64 << 10;
+bool tma_ok(const mp_engine_opts& o, bool peer) {
+  return !(o.tma_peer < 0 || (peer && o.tma_peer == 0));
+}
+bool vec_peer(const mp_engine_opts& o, bool peer) { return o.copy_kind == MP_COPY_TMA && !tma_ok(o, peer); }
+
+// Launch the transfer kernel (mp_kernels.cuh) over one tile table.
 // `nstatic` > 0 only for tables without flag waits: static first tiles must
 // never be waited on by another CTA (residency of every CTA is not guaranteed).
 void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, const mpk::Tile* tiles,
                      unsigned ntiles, mpk::Ctl* ctl, unsigned nstatic,
                      unsigned long long* trace = nullptr, const mpk::GroupSync* gsync = nullptr,
-                     bool peer = false, int sms = 148, const mpk::SmallTable* small = nullptr) {
-  if (small && !trace && !gsync) {  // small static direct table: one-slot kernel
+                     bool peer = false, int sms = 148, const mpk::SmallTable* small = nullptr,
+                     int kind = PROG_DYNAMIC) {
+  if (kind == PROG_SMALL && small && !trace && !gsync) {
     mpk::small_copy_kernel<4><<<ntiles, 256, 0, s>>>(*small);
     CK(cudaGetLastError());
     return;
   }
   mp_engine_opts o = o_in;
-  if ((o.tma_peer < 0 || (peer && o.tma_peer == 0)) && o.copy_kind == MP_COPY_TMA) {
-    // (tma_peer < 0 forces this path on every table: single-GPU testing)
-    // NVLink peer tables: the 16-byte LDG/STG kernel (2 x 256 threads per SM)
+  if (kind != PROG_DYNAMIC && tma_ok(o, peer)) {
+    // static table (a traced small one too): the TMA ring, one CTA per tile
+    o.copy_kind = MP_COPY_TMA;
+    o.threads = 128;
+  } else if (kind != PROG_DYNAMIC || vec_peer(o, peer)) {
+    // LDG/STG kernel at the measured shape (tma_peer < 0 forces it: testing)
     o.copy_kind = MP_COPY_VEC;
     o.unroll = 8;
     o.threads = 256;
-    grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sms * 2);
+    grid = (unsigned)std::min<uint64_t>(ntiles, (uint64_t)sms * kPeerCtasPerSm);
     nstatic = nstatic ? grid : 0;
   }
   KernelFn fn = pick_kernel(o);
@@ -149,7 +175,8 @@ struct Program {
   unsigned grid = 0;
   unsigned nstatic = 0;  // = grid when the table has no flag waits
   bool peer = false;     // some tile reads or writes another GPU's memory
-  std::shared_ptr<mpk::SmallTable> small;  // small static direct table (kernel params)
+  int kind = PROG_DYNAMIC;                 // ProgKind
+  std::shared_ptr<mpk::SmallTable> small;  // PROG_SMALL: the table as kernel params
 };
 
 struct Entry {
@@ -468,7 +495,34 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
   // still yields <= grid tiles.  The kernel then runs with no claim atomics
   // and no exit protocol (mp_kernels.cuh); every CTA streams an equal share.
   // Devices with waits or PCIe tiles keep dynamic claims (load balance).
+  // tables that touch another GPU's memory over NVLink (see launch_transfer)
+  std::vector<char> peer_phys(ctx->phys.size(), 0);
+  for (int t = 0; t < T; ++t) {
+    const int sp = ctx->logi[xs[t].sd].phys, dp = ctx->logi[xs[t].dd].phys;
+    if (sp != dp) peer_phys[o.pull ? dp : sp] = 1;
+    for (const mp_path& P : xs[t].paths)
+      if (P.kind == MP_PATH_GPU) {
+        const int rp = ctx->logi[P.stage].phys;
+        if (rp != sp) peer_phys[sp] = 1;
+        if (rp != dp) peer_phys[rp] = 1;
+      }
+  }
+  // CTAs of a device's dynamic kernel
+  auto grid_of = [&](size_t ph) {
+    int per_sm = vec_peer(o, peer_phys[ph] != 0) ? kPeerCtasPerSm : std::max(1, o.ctas_per_sm);
+    if (o.copy_kind == MP_COPY_TMA && !vec_peer(o, peer_phys[ph] != 0))  // rings that fit one SM
+      per_sm = std::min<int>(per_sm, std::max<int>(1, (int)((227u << 10) / kernel_smem(o))));
+    return (uint64_t)ctx->phys[ph].sms * per_sm;
+  };
+
+  // Static schedule (MP_SCHED_AUTO): a device whose tiles never wait on a flag
+  // and never touch host memory, and whose share is <= kStaticMaxPerCta per
+  // SM, gets ONE tile per SM — tile bytes = its SM bytes over (SMs - 2 x
+  // segments), so cutting every chunk-hop segment still yields <= SMs tiles.
+  // Those kernels run with no claim atomics and no exit protocol.  Devices
+  // with waits or PCIe tiles keep dynamic claims (load balance).
   std::vector<uint64_t> static_tile(ctx->phys.size(), 0);
+  std::vector<int> static_kind(ctx->phys.size(), PROG_DYNAMIC);
   if (o.sched == MP_SCHED_AUTO && o.tile_bytes == 0) {
     const size_t nph = ctx->phys.size();
     std::vector<uint64_t> sm_bytes(nph, 0);
@@ -492,21 +546,25 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
       }
     }
     for (size_t ph = 0; ph < nph; ++ph) {
-      const uint64_t grid = (uint64_t)ctx->phys[ph].sms * std::max(1, o.ctas_per_sm);
-      if (dyn[ph] || segs[ph] == 0 || (uint64_t)segs[ph] * 4 > grid ||
-          sm_bytes[ph] > grid * kStaticMaxPerCta)
-        continue;
+      const uint64_t grid = (uint64_t)ctx->phys[ph].sms;
+      if (dyn[ph] || segs[ph] == 0 || (uint64_t)segs[ph] * 4 > grid) continue;
+      const bool small = sm_bytes[ph] <= (uint64_t)o.small_max_bytes;
+      const bool tma = sm_bytes[ph] <= grid * kStaticMaxPerCta && tma_ok(o, peer_phys[ph] != 0);
+      if (!small && !tma) continue;
       uint64_t tb = (sm_bytes[ph] + (grid - 2 * segs[ph]) - 1) / (grid - 2 * segs[ph]);
       tb = std::max<uint64_t>(tb, kStaticMinTile);
       static_tile[ph] = (tb + 15) & ~(uint64_t)15;
+      static_kind[ph] = small ? PROG_SMALL : PROG_STATIC_TMA;
     }
   }
   auto tile_for = [&](int ph, uint64_t path_bytes) {
-    return static_tile[ph] ? static_tile[ph] : auto_tile_bytes(ctx, path_bytes, ctx->phys[ph].sms);
+    if (static_tile[ph]) return static_tile[ph];
+    if (o.tile_bytes == 0 && (o.copy_kind == MP_COPY_VEC || vec_peer(o, peer_phys[ph] != 0)))
+      return kVecTileBytes;
+    return auto_tile_bytes(ctx, path_bytes, ctx->phys[ph].sms);
   };
 
   std::vector<std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>> tiles(ctx->phys.size());
-  std::vector<char> peer_phys(ctx->phys.size(), 0);
   std::vector<uint64_t> stage_cursor(ctx->logi.size(), 0);  // shared relay arenas
   uint64_t host_cursor = 0;                                  // shared pinned arena
   auto new_event = [&](int phys) {
@@ -521,14 +579,6 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
     const int np = (int)paths.size(), nc = (int)chunks[t].size();
     const int sp = ctx->logi[x.sd].phys, dp = ctx->logi[x.dd].phys;
     const uint64_t s0 = (uint64_t)(uintptr_t)x.src, d0 = (uint64_t)(uintptr_t)x.dst;
-    // tables that touch another GPU's memory over NVLink (see launch_transfer)
-    if (sp != dp) peer_phys[o.pull ? dp : sp] = 1;
-    for (const mp_path& P : paths)
-      if (P.kind == MP_PATH_GPU) {
-        const int rp = ctx->logi[P.stage].phys;
-        if (rp != sp) peer_phys[sp] = 1;
-        if (rp != dp) peer_phys[rp] = 1;
-      }
     std::vector<int> lane_base(np, 0);
     for (int p = 0; p < np; ++p) {
       lane_base[p] = lane_next;
@@ -668,23 +718,22 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
     pr.phys = (int)ph;
     pr.ntiles = (unsigned)flat.size();
     Phys& P = ctx->phys[ph];
-    pr.grid = (unsigned)std::min<uint64_t>(flat.size(), (uint64_t)P.sms * std::max(1, o.ctas_per_sm));
-    bool waits = false;
-    for (const auto& tl : flat) waits |= tl.wait != nullptr;
-    pr.nstatic = waits ? 0u : pr.grid;
+    bool waits = false, plain = true;
+    for (const auto& tl : flat) {
+      waits |= tl.wait != nullptr;
+      plain = plain && !tl.wait && !tl.signal && tl.flags == 0;
+    }
     pr.peer = peer_phys[ph] != 0;
+    pr.kind = static_tile[ph] && flat.size() <= (size_t)P.sms ? static_kind[ph] : PROG_DYNAMIC;
+    if (pr.kind == PROG_SMALL && (!plain || flat.size() > mpk::kSmallMaxTiles))
+      pr.kind = tma_ok(o, pr.peer) ? PROG_STATIC_TMA : PROG_DYNAMIC;  // e.g. relay hop1 tiles
+    pr.grid = (unsigned)std::min<uint64_t>(flat.size(), pr.kind == PROG_DYNAMIC ? grid_of(ph) : P.sms);
+    pr.nstatic = waits ? 0u : pr.grid;
     CK(cudaSetDevice(P.ordinal));
     CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile)));
     e->progs.push_back(pr);  // owned by the entry from here (freed on error)
     CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
-    // small static table of plain direct tiles: the one-slot small kernel
-    uint64_t tbytes = 0;
-    bool plain = flat.size() <= mpk::kSmallMaxTiles;
-    for (const auto& tl : flat) {
-      tbytes += tl.len;
-      plain = plain && !tl.wait && !tl.signal && tl.flags == 0;
-    }
-    if (plain && o.sched == MP_SCHED_AUTO && tbytes <= (uint64_t)o.small_max_bytes) {
+    if (pr.kind == PROG_SMALL) {
       auto sm = std::make_shared<mpk::SmallTable>();
       for (size_t i = 0; i < flat.size(); ++i) {
         sm->src[i] = flat[i].src;
@@ -737,7 +786,7 @@ void enqueue_group(mp_ctx* ctx, Entry* e, cudaStream_t origin) {
   if (!e->progs.empty()) {
     const Program& pr = e->progs[0];
     launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic, nullptr, &g,
-                    pr.peer, P.sms, pr.small.get());
+                    pr.peer, P.sms, pr.small.get(), pr.kind);
   } else if (e->grole == 3) {
     mpk::group_recv_kernel<<<1, 32, 0, P.kstream>>>(g, ctx->group->done(ctx->group->rank), e->expected,
                                                     P.ctl);
@@ -788,7 +837,7 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr 
     if (t) ctx->timed_phys = pr.phys;
     if (t) CK(cudaEventRecord(P.kt0, P.kstream));
     launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic,
-                    tr ? tr->stamps[pr.phys] : nullptr, nullptr, pr.peer, P.sms, pr.small.get());
+                    tr ? tr->stamps[pr.phys] : nullptr, nullptr, pr.peer, P.sms, pr.small.get(), pr.kind);
     if (t) CK(cudaEventRecord(P.kt1, P.kstream));
   }
   // copy-engine lanes
@@ -1064,11 +1113,13 @@ int mp_ctx_create(int32_t n_logical, const int32_t* device_map, mp_ctx** out) {
   auto ctx = std::make_unique<mp_ctx>();
   ctx->opts.direct_engine = MP_ENGINE_SM;
   ctx->opts.relay_engine = MP_ENGINE_SM;
-  // measured defaults (profiles/r01_kernel_sweep.jsonl): TMA bulk ring of
-  // 4 x 32 KiB, one CTA per SM, reaches 98% of the measured HBM copy peak
-  ctx->opts.copy_kind = MP_COPY_TMA;
-  ctx->opts.ctas_per_sm = 1;
-  ctx->opts.threads = 128;
+  // measured defaults (tools/abi_latency.cu, profiles/): dynamic tables run
+  // the LDG/STG kernel, 4 CTAs x 256 threads per SM, 64 KiB tiles (100% of
+  // the measured HBM copy peak at 512 MiB); static tables run the TMA ring
+  // (4 x 32 KiB per SM) and small ones the small-message kernel
+  ctx->opts.copy_kind = MP_COPY_VEC;
+  ctx->opts.ctas_per_sm = 4;
+  ctx->opts.threads = 256;
   ctx->opts.tile_bytes = 0;
   ctx->opts.host_slots = 0;
   ctx->opts.pull = 0;
@@ -1549,11 +1600,11 @@ int mp_kernel_bench(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int3
   CK(cudaSetDevice(S.ordinal));
   CK(cudaDeviceSynchronize());
   launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
-                  nullptr, pr->peer, S.sms, pr->small.get());  // warm
+                  nullptr, pr->peer, S.sms, pr->small.get(), pr->kind);  // warm
   CK(cudaEventRecord(S.kt0, S.kstream));
   for (int i = 0; i < reps; ++i)
     launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
-                    nullptr, pr->peer, S.sms, pr->small.get());
+                    nullptr, pr->peer, S.sms, pr->small.get(), pr->kind);
   CK(cudaEventRecord(S.kt1, S.kstream));
   CK(cudaEventSynchronize(S.kt1));
   float ms = 0.f;

@@ -172,8 +172,7 @@ class Engine:
     def send_ptr(self, src_ptr: int, dst_ptr: int, nbytes: int, src_dev: int, dst_dev: int,
                  config: PathConfig, stream: int = 0) -> None:
         """Raw-pointer send through the C ABI (`mp_send`)."""
-        cfg = config.abi()
-        check(lib.mp_send(self._ctx, src_ptr, dst_ptr, nbytes, src_dev, dst_dev, C.byref(cfg),
+        check(lib.mp_send(self._ctx, src_ptr, dst_ptr, nbytes, src_dev, dst_dev, config.abi_ref(),
                           stream or None))
 
     def send(self, src, dst, nbytes: int | None = None, config: PathConfig | None = None,
@@ -184,31 +183,34 @@ class Engine:
         device): ordered after prior work there, and that stream waits for
         completion.  `src_dev`/`dst_dev` are logical accelerators; by default
         the first logical device mapped to each tensor's GPU.
+        (Kept lean: on a cached-graph hit this Python is most of the host cost.)
         """
-        torch = _torch()
-        config = config or PathConfig.from_env()
+        if config is None:
+            config = PathConfig.from_env()
+        sn = src.nbytes
         if nbytes is None:
-            nbytes = src.numel() * src.element_size()
-        if nbytes > dst.numel() * dst.element_size() or nbytes > src.numel() * src.element_size():
+            nbytes = sn
+        if nbytes > sn or nbytes > dst.nbytes:
             raise ValueError("nbytes exceeds a buffer")
+        sp, dp = src.get_device(), dst.get_device()
+        dmap = self.device_map
         if src_dev is None:
-            src_dev = self.device_map.index(src.device.index)
+            if sp not in dmap:
+                raise ValueError(f"src lives on cuda:{sp}, which no logical device maps to")
+            src_dev = dmap.index(sp)
         if dst_dev is None:
-            phys = dst.device.index
-            cands = [i for i, d in enumerate(self.device_map) if d == phys and i != src_dev]
+            cands = [i for i, d in enumerate(dmap) if d == dp and i != src_dev]
             if not cands:
                 raise ValueError("cannot infer the logical destination device; pass dst_dev")
             dst_dev = cands[0]
-        if (src.device.index, dst.device.index) != (self.device_map[src_dev],
-                                                    self.device_map[dst_dev]):
-            raise ValueError(f"src/dst tensors live on cuda:{src.device.index}/"
-                             f"cuda:{dst.device.index}, but logical devices {src_dev}/{dst_dev} "
-                             f"map to cuda:{self.device_map[src_dev]}/"
-                             f"cuda:{self.device_map[dst_dev]}")
+        if dmap[src_dev] != sp or dmap[dst_dev] != dp:
+            raise ValueError(f"src/dst tensors live on cuda:{sp}/cuda:{dp}, but logical devices "
+                             f"{src_dev}/{dst_dev} map to cuda:{dmap[src_dev]}/cuda:{dmap[dst_dev]}")
         if stream is None:
-            stream = torch.cuda.current_stream(src.device)
+            stream = _torch().cuda.current_stream(sp)
         handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
-        self.send_ptr(src.data_ptr(), dst.data_ptr(), nbytes, src_dev, dst_dev, config, handle)
+        check(lib.mp_send(self._ctx, src.data_ptr(), dst.data_ptr(), nbytes, src_dev, dst_dev,
+                          config.abi_ref(), handle or None))
 
     def send_many(self, transfers, config: PathConfig | None = None, joint: bool = False,
                   stream=None) -> None:

@@ -104,7 +104,9 @@ int main(int argc, char** argv) {
   const char* variant = getenv("ENGINE");
   mp_engine_opts o = base;
   if (variant && variant[0] == 'v') { o.copy_kind = MP_COPY_VEC; o.threads = 256; }
+  if (variant && variant[0] == 'r') { o.copy_kind = MP_COPY_TMA; o.threads = 128; o.ctas_per_sm = 1; }
   if (variant && variant[0] == 'c') o.direct_engine = MP_ENGINE_CE;
+  if (variant && variant[0] == 'p') o.tma_peer = -1; /* the NVLink-peer LDG/STG kernel */
   if (getenv("SMALL")) o.small_max_bytes = atoll(getenv("SMALL"));
   const char* sched = getenv("SCHED");
   if (sched && sched[0] == 'd') o.sched = MP_SCHED_DYNAMIC;
@@ -136,7 +138,7 @@ int main(int argc, char** argv) {
       CHECK(mp_send_stats_get(ctx, &st));
       printf("{\"engine\": \"%s%s small<=%lld\", \"mode\": \"%s\", \"bytes\": %llu, \"host_us_mean\": %.3f, \"host_us_p50\": %.3f, "
              "\"host_us_p99\": %.3f, \"gpu_us_per_msg\": %.3f, \"gbs\": %.3f, \"launch_us\": %.3f}\n",
-             variant ? variant : "tma", o.sched == MP_SCHED_DYNAMIC ? "+dynamic" : "", (long long)o.small_max_bytes, mode == 0 ? "single_graph" : mode == 1 ? "multi_graph" : "single_stream",
+             variant ? variant : "default", o.sched == MP_SCHED_DYNAMIC ? "+dynamic" : "", (long long)o.small_max_bytes, mode == 0 ? "single_graph" : mode == 1 ? "multi_graph" : "single_stream",
              (unsigned long long)n, sum / it, per[it / 2], per[(int)(it * 0.99)],
              ms * 1e3 / it, n / (ms * 1e-3 / it) / 1e9, st.launch_us);
       fflush(stdout);
