@@ -157,7 +157,13 @@ typedef struct {
   double launch_us;          /* host time of the enqueue call         */
   double plan_us;            /* plan + key on a miss                  */
   uint64_t cache_hits, cache_misses, cache_evictions;
+  int32_t kernel;            /* MP_KERNEL_*: the source device's copy kernel */
+  int32_t pad;
 } mp_send_stats;
+#define MP_KERNEL_NONE (-1)  /* copy engines only                           */
+#define MP_KERNEL_VEC 0      /* transfer_kernel<0,U>: 16-byte LDG/STG        */
+#define MP_KERNEL_TMA 1      /* transfer_kernel<1,8>: TMA bulk ring          */
+#define MP_KERNEL_SMALL 2    /* small_copy_kernel: descriptors in params     */
 
 /* Engine knobs (choice of copy mechanism per path type; measured defaults). */
 #define MP_ENGINE_SM 0       /* hand-written sm_100a copy kernel       */

@@ -92,7 +92,8 @@ class mp_send_stats(C.Structure):
                 ("creation_us", C.c_double), ("construction_us", C.c_double),
                 ("instantiation_us", C.c_double), ("launch_us", C.c_double),
                 ("plan_us", C.c_double), ("cache_hits", C.c_uint64),
-                ("cache_misses", C.c_uint64), ("cache_evictions", C.c_uint64)]
+                ("cache_misses", C.c_uint64), ("cache_evictions", C.c_uint64),
+                ("kernel", C.c_int32), ("pad", C.c_int32)]
 
 
 class mp_trace_rec(C.Structure):

@@ -86,6 +86,14 @@ bool tma_ok(const mp_engine_opts& o, bool peer) {
 }
 bool vec_peer(const mp_engine_opts& o, bool peer) { return o.copy_kind == MP_COPY_TMA && !tma_ok(o, peer); }
 
+// Which kernel launch_transfer runs for a table (MP_KERNEL_*, untraced).
+int kernel_of(const mp_engine_opts& o, int kind, bool peer) {
+  if (kind == PROG_SMALL) return MP_KERNEL_SMALL;
+  if (kind != PROG_DYNAMIC) return tma_ok(o, peer) ? MP_KERNEL_TMA : MP_KERNEL_VEC;
+  if (vec_peer(o, peer)) return MP_KERNEL_VEC;
+  return o.copy_kind == MP_COPY_TMA ? MP_KERNEL_TMA : MP_KERNEL_VEC;
+}
+
 // Launch the transfer kernel (mp_kernels.cuh) over one tile table.
 // `nstatic` > 0 only for tables without flag waits: static first tiles must
 // never be waited on by another CTA (residency of every CTA is not guaranteed).
@@ -716,7 +724,6 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
     for (auto& kv : v) flat.push_back(kv.second);
     Program pr;
     pr.phys = (int)ph;
-    pr.ntiles = (unsigned)flat.size();
     Phys& P = ctx->phys[ph];
     bool waits = false, plain = true;
     for (const auto& tl : flat) {
@@ -727,6 +734,7 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
     pr.kind = static_tile[ph] && flat.size() <= (size_t)P.sms ? static_kind[ph] : PROG_DYNAMIC;
     if (pr.kind == PROG_SMALL && (!plain || flat.size() > mpk::kSmallMaxTiles))
       pr.kind = tma_ok(o, pr.peer) ? PROG_STATIC_TMA : PROG_DYNAMIC;  // e.g. relay hop1 tiles
+    pr.ntiles = (unsigned)flat.size();
     pr.grid = (unsigned)std::min<uint64_t>(flat.size(), pr.kind == PROG_DYNAMIC ? grid_of(ph) : P.sms);
     pr.nstatic = waits ? 0u : pr.grid;
     CK(cudaSetDevice(P.ordinal));
@@ -1338,6 +1346,9 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
   st.nodes_logical = e->nodes_logical;
   st.nodes_physical = e->nodes_physical;
   st.kernels = (int)e->progs.size();
+  st.kernel = MP_KERNEL_NONE;
+  for (const Program& pr : e->progs)
+    if (pr.phys == e->src_phys) st.kernel = kernel_of(ctx->opts, pr.kind, pr.peer);
   ctx->last_paths = e->paths;
   ctx->last_chunks = e->chunks;
   return MP_OK;
@@ -1394,6 +1405,9 @@ int mp_send_many(mp_ctx* ctx, const mp_xfer* xfers, int32_t n, const mp_config* 
   st.nodes_physical = e->nodes_physical;
   st.kernels = (int)e->progs.size();
   st.ce_copies = (int)e->ce.size();
+  st.kernel = MP_KERNEL_NONE;
+  for (const Program& pr : e->progs)
+    if (pr.phys == e->src_phys) st.kernel = kernel_of(ctx->opts, pr.kind, pr.peer);
   ctx->last_paths = e->paths;
   ctx->last_chunks = e->chunks;
   return MP_OK;
@@ -1928,6 +1942,7 @@ int mp_group_send(mp_ctx* ctx, const void* src, uint32_t src_align, void* dst, u
   st.nodes_physical = e->nodes_physical;
   st.kernels = 1;
   st.ce_copies = 0;
+  st.kernel = e->progs.empty() ? MP_KERNEL_NONE : kernel_of(ctx->opts, e->progs[0].kind, e->progs[0].peer);
   ctx->last_paths = e->paths;
   ctx->last_chunks = e->chunks;
   return MP_OK;

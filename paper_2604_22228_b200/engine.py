@@ -28,6 +28,9 @@ from .topology import Topology, load_topology, mesh_text
 
 ENGINES = {"sm": MP_ENGINE_SM, "ce": MP_ENGINE_CE}
 COPIES = {"vec": MP_COPY_VEC, "tma": MP_COPY_TMA}
+KERNELS = {0: "mpk::transfer_kernel<0,8> (16-byte LDG/STG, dynamic tile claims)",
+           1: "mpk::transfer_kernel<1,8> (TMA bulk ring)",
+           2: "mpk::small_copy_kernel<4> (descriptors in kernel params)"}
 
 
 @dataclass
@@ -48,6 +51,7 @@ class SendStats:
     cache_hits: int
     cache_misses: int
     cache_evictions: int
+    kernel: str = ""  # the source device's copy kernel ("" = copy engines only)
 
 
 def _torch():
@@ -255,7 +259,7 @@ class Engine:
         return SendStats(bool(s.hit), bool(s.graph_mode), s.nodes_logical, s.nodes_physical,
                          s.kernels, s.ce_copies, s.creation_us, s.construction_us,
                          s.instantiation_us, s.launch_us, s.plan_us, s.cache_hits,
-                         s.cache_misses, s.cache_evictions)
+                         s.cache_misses, s.cache_evictions, KERNELS.get(s.kernel, ""))
 
     def last_plan(self):
         """(paths, chunks) the engine executed on the last send — for parity checks."""

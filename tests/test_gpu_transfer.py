@@ -232,3 +232,19 @@ def test_tile_schedules(mode, size, chunks, host, offs):
     _check(eng, text, size, host=host, chunks=chunks, graph=True, src_off=offs[0],
            dst_off=offs[1], seed=11, reps=2)
     eng.close()
+
+
+@pytest.mark.parametrize("size,opts,kernel", [
+    (4096, {}, "small_copy_kernel"), (4 * MiB, {}, "small_copy_kernel"),
+    (32 * MiB, {}, "transfer_kernel<1,8>"), (160 * MiB, {}, "transfer_kernel<0,8>"),
+    (32 * MiB, {"tma_peer": -1}, "transfer_kernel<0,8>"),
+    (32 * MiB, {"small_max_bytes": 64 << 20}, "small_copy_kernel"),
+    (4096, {"sched": "dynamic"}, "transfer_kernel<0,8>"),
+    (160 * MiB, {"copy": "tma", "ctas_per_sm": 1, "threads": 128}, "transfer_kernel<1,8>")])
+def test_kernel_choice_by_size(size, opts, kernel):
+    """The measured per-table kernel policy (csrc/mp_engine.cu ProgKind),
+    reported by the send statistics, delivering exact bytes."""
+    eng, text = _engine(2, **opts)
+    st = _check(eng, text, size, graph=True, seed=5)
+    assert kernel in st.kernel, st.kernel
+    eng.close()
