@@ -363,7 +363,10 @@ int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t byt
                      int32_t iters, double* out_gbps, int32_t cap);
 
 /* Device time of the transfer kernel of the last streamed-mode send (CUDA
- * events on its stream around that one launch, launch latency included). */
+ * events on its stream around that one launch, launch latency included).
+ * Off by default (timing events cost ~2 launch slots per send): enable with
+ * mp_ctx_set_kernel_timing(ctx, 1). */
+int mp_ctx_set_kernel_timing(mp_ctx* ctx, int32_t on);
 int mp_kernel_time_ms(const mp_ctx* ctx, double* ms);
 /* Average duration of the src device's transfer kernel for this transfer's
  * program over `reps` back-to-back launches between two CUDA events on its

@@ -173,6 +173,7 @@ SIGNATURES = {
     "mp_sync": (C.c_int, [_vp]),
     "mp_measure_paths": (C.c_int, [_vp, _i32, _i32, _u64, _i32, P(C.c_double), _i32]),
     "mp_kernel_time_ms": (C.c_int, [_vp, P(C.c_double)]),
+    "mp_ctx_set_kernel_timing": (C.c_int, [_vp, _i32]),
     "mp_kernel_bench": (C.c_int, [_vp, _vp, _vp, _u64, _i32, _i32, P(mp_config), _i32,
                                   P(C.c_double)]),
     "mp_ipc_export": (C.c_int, [_vp, _i32, P(C.c_uint8), P(_u64)]),

@@ -86,6 +86,21 @@ bool tma_ok(const mp_engine_opts& o, bool peer) {
 }
 bool vec_peer(const mp_engine_opts& o, bool peer) { return o.copy_kind == MP_COPY_TMA && !tma_ok(o, peer); }
 
+// Raise a kernel's dynamic shared-memory limit on the current device once
+// (cudaFuncSetAttribute costs microseconds; a per-launch call would dominate
+// a small message's host time).
+void allow_smem(KernelFn fn, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, KernelFn>, size_t> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{dev, fn}];
+  if (have >= smem) return;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  have = smem;
+}
+
 // Which kernel launch_transfer runs for a table (MP_KERNEL_*, untraced).
 int kernel_of(const mp_engine_opts& o, int kind, bool peer) {
   if (kind == PROG_SMALL) return MP_KERNEL_SMALL;
@@ -100,10 +115,18 @@ int kernel_of(const mp_engine_opts& o, int kind, bool peer) {
 void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, const mpk::Tile* tiles,
                      unsigned ntiles, mpk::Ctl* ctl, unsigned nstatic,
                      unsigned long long* trace = nullptr, const mpk::GroupSync* gsync = nullptr,
-                     bool peer = false, int sms = 148, const mpk::SmallTable* small = nullptr,
+                     bool peer = false, int sms = 148, const mpk::SmallTable<mpk::kSmallMaxTiles>* small = nullptr,
                      int kind = PROG_DYNAMIC) {
   if (kind == PROG_SMALL && small && !trace && !gsync) {
-    mpk::small_copy_kernel<4><<<ntiles, 256, 0, s>>>(*small);
+    if (ntiles <= mpk::kSmallTilesLo) {
+      mpk::SmallTable<mpk::kSmallTilesLo> lo;
+      std::copy(small->src, small->src + ntiles, lo.src);
+      std::copy(small->dst, small->dst + ntiles, lo.dst);
+      std::copy(small->len, small->len + ntiles, lo.len);
+      mpk::small_copy_kernel<4, mpk::kSmallTilesLo><<<ntiles, 256, 0, s>>>(lo);
+    } else {
+      mpk::small_copy_kernel<4, mpk::kSmallMaxTiles><<<ntiles, 256, 0, s>>>(*small);
+    }
     CK(cudaGetLastError());
     return;
   }
@@ -122,7 +145,7 @@ void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, 
   }
   KernelFn fn = pick_kernel(o);
   size_t smem = kernel_smem(o);
-  if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (smem > 48 * 1024) allow_smem(fn, smem);
   mpk::GroupSync g{};
   if (gsync) g = *gsync;
   fn<<<grid, o.threads, smem, s>>>(tiles, ntiles, ctl, (unsigned)o.tma_stages, (unsigned)o.tma_block,
@@ -184,7 +207,7 @@ struct Program {
   unsigned nstatic = 0;  // = grid when the table has no flag waits
   bool peer = false;     // some tile reads or writes another GPU's memory
   int kind = PROG_DYNAMIC;                 // ProgKind
-  std::shared_ptr<mpk::SmallTable> small;  // PROG_SMALL: the table as kernel params
+  std::shared_ptr<mpk::SmallTable<mpk::kSmallMaxTiles>> small;  // PROG_SMALL: the table as kernel params
 };
 
 struct Entry {
@@ -243,6 +266,7 @@ struct mp_ctx {
   void* last_stream = nullptr;
   bool have_last = false;
   int timed_phys = -1;  // device whose kt0/kt1 events bracket the last timed kernel
+  bool kernel_timing = false;  // streamed sends bracket the kernel with kt0/kt1
   struct SizeRule {
     uint64_t max_bytes;
     int direct, host;  // MP_ENGINE_*, host -1 = opts.host_engine
@@ -742,7 +766,7 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
     e->progs.push_back(pr);  // owned by the entry from here (freed on error)
     CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
     if (pr.kind == PROG_SMALL) {
-      auto sm = std::make_shared<mpk::SmallTable>();
+      auto sm = std::make_shared<mpk::SmallTable<mpk::kSmallMaxTiles>>();
       for (size_t i = 0; i < flat.size(); ++i) {
         sm->src[i] = flat[i].src;
         sm->dst[i] = flat[i].dst;
@@ -814,8 +838,20 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr 
     return;
   }
   Phys& S = ctx->phys[e->src_phys];
-  for (auto& p : ctx->phys) p.next_event = 0;
   CK(cudaSetDevice(S.ordinal));
+  if (!tr && e->ce.empty() && e->progs.size() == 1 && e->progs[0].phys == e->src_phys) {
+    // one kernel on the caller's device and nothing else: no fork/join, the
+    // kernel goes straight onto the caller's stream (per-call launch ~= one
+    // kernel launch; a captured graph is the single kernel node either way)
+    const Program& pr = e->progs[0];
+    if (timing) ctx->timed_phys = pr.phys;
+    if (timing) CK(cudaEventRecord(S.kt0, origin));
+    launch_transfer(ctx->opts, pr.grid, origin, pr.d_tiles, pr.ntiles, S.ctl, pr.nstatic, nullptr,
+                    nullptr, pr.peer, S.sms, pr.small.get(), pr.kind);
+    if (timing) CK(cudaEventRecord(S.kt1, origin));
+    return;
+  }
+  for (auto& p : ctx->phys) p.next_event = 0;
   cudaEvent_t fork = take_event(S);
   CK(cudaEventRecord(fork, origin));
   std::vector<std::pair<int, cudaStream_t>> used;
@@ -1330,7 +1366,7 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
   // serialise with a send issued on another stream (shared counters/arenas)
   if (ctx->have_last && ctx->last_stream != stream) CK(cudaStreamWaitEvent(user, ctx->last_done, 0));
   double t_launch = now_us();
-  bool timing = !cfg->graph_mode;
+  bool timing = !cfg->graph_mode && ctx->kernel_timing;
   if (cfg->graph_mode && e->graph) {
     CK(cudaGraphLaunch(e->exec, user));
     st.ce_copies = (int)e->ce.size();
@@ -1574,6 +1610,13 @@ int mp_sync(mp_ctx* ctx) {
   }
   return MP_OK;
   GUARD_END
+}
+
+int mp_ctx_set_kernel_timing(mp_ctx* ctx, int32_t on) {
+  if (!ctx) return fail(MP_ERR_VALUE, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  ctx->kernel_timing = on != 0;
+  return MP_OK;
 }
 
 int mp_kernel_time_ms(const mp_ctx* ctx, double* ms) {

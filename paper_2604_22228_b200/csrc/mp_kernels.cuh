@@ -445,14 +445,18 @@ struct TmaEngine {
 // tiles only (no flags, no host memory), one tile per CTA.
 // ---------------------------------------------------------------------------
 constexpr unsigned kSmallMaxTiles = 148;
+template <unsigned N>
 struct SmallTable {
-  uint64_t src[kSmallMaxTiles];
-  uint64_t dst[kSmallMaxTiles];
-  uint32_t len[kSmallMaxTiles];
+  uint64_t src[N];
+  uint64_t dst[N];
+  uint32_t len[N];
 };
+// Parameter block sizes: a launch copies its parameters, so tables of up to
+// 16 tiles (messages <= 64 KiB at 4 KiB tiles) use a 320-byte block.
+constexpr unsigned kSmallTilesLo = 16;
 
-template <int V>
-__global__ void __launch_bounds__(256) small_copy_kernel(const __grid_constant__ SmallTable tab) {
+template <int V, unsigned N>
+__global__ void __launch_bounds__(256) small_copy_kernel(const __grid_constant__ SmallTable<N> tab) {
   const uint8_t* src = (const uint8_t*)tab.src[blockIdx.x];
   uint8_t* dst = (uint8_t*)tab.dst[blockIdx.x];
   const uint32_t len = tab.len[blockIdx.x];

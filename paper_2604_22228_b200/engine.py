@@ -308,6 +308,11 @@ class Engine:
     def clear_cache(self) -> None:
         check(lib.mp_cache_clear(self._ctx))
 
+    def set_kernel_timing(self, on: bool = True) -> None:
+        """Bracket every streamed-mode send's kernel with CUDA events (off by
+        default: the events cost launch slots) so `kernel_time_ms` works."""
+        check(lib.mp_ctx_set_kernel_timing(self._ctx, int(on)))
+
     def kernel_time_ms(self) -> float:
         ms = C.c_double()
         check(lib.mp_kernel_time_ms(self._ctx, C.byref(ms)))

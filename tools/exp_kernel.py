@@ -54,6 +54,7 @@ def send_rate(eng, cfg, size=S, reps=10):
 
 single = PathConfig(max_chunks=1, graph_mode=False)
 eng = Engine.loopback(2)
+eng.set_kernel_timing(True)
 
 # 1. vec variants
 for unroll in (4, 8, 16):

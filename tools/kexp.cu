@@ -136,14 +136,14 @@ int main() {
              k_vec<<<nt, 256, 0, s>>>(dt, nt, ctl, 4, 32768, nt, nullptr, gs);
            }));
     {
-      static mpk::SmallTable st;
+      static mpk::SmallTable<mpk::kSmallMaxTiles> st;
       for (unsigned i = 0; i < nt; ++i) {
         st.src[i] = tv[i].src;
         st.dst[i] = tv[i].dst;
         st.len[i] = (uint32_t)tv[i].len;
       }
       printf("small %8u B %3u tiles     %.3f us\n", bytes, nt,
-             per_launch_us(s, [&] { mpk::small_copy_kernel<4><<<nt, 256, 0, s>>>(st); }));
+             per_launch_us(s, [&] { mpk::small_copy_kernel<4, mpk::kSmallMaxTiles><<<nt, 256, 0, s>>>(st); }));
     }
     printf("tma %8u B ntiles=0        %.3f us\n", bytes, per_launch_us(s, [&] {
              k_tma<<<nt, 128, 4 * 32768, s>>>(dt, 0, ctl, 4, 32768, 0, nullptr, gs);

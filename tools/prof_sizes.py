@@ -15,6 +15,7 @@ sizes = [int(x) for x in os.environ.get("SIZES", "").split(",") if x] or \
     [1 * MiB, 4 * MiB, 16 * MiB, 32 * MiB, 64 * MiB, 128 * MiB, 512 * MiB]
 reps = int(os.environ.get("REPS", 20))
 eng = Engine.loopback(2)
+eng.set_kernel_timing(True)
 opts = os.environ.get("ENGINE_OPTS")
 if opts:
     eng.configure(**json.loads(opts))
