@@ -6,7 +6,9 @@ The planner TU (mp_core.cpp) is compiled by g++ with -ffp-contract=off and no
 fast-math so its float arithmetic rounds exactly like CPython's; the engine TU
 (mp_engine.cu) by nvcc for `-gencode arch=compute_100a,code=sm_100a` with
 -lineinfo.  cudart is linked statically, so the library loads (and its
-planner entry points work) on a machine without a GPU.
+planner entry points work) on a machine without a GPU.  `_mpfast` is the
+CPython fast path of the per-message send (csrc/mp_pyfast.c), linked against
+the library.
 """
 
 from __future__ import annotations
@@ -15,6 +17,7 @@ import os
 import shutil
 import subprocess
 import sys
+import sysconfig
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -22,6 +25,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libmpb200.so")
+FAST = os.path.join(PKG, "_mpfast" + sysconfig.get_config_var("EXT_SUFFIX"))
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -66,6 +70,12 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
     if force or _stale(LIB, [core_obj, eng_obj]):
         _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", LIB, core_obj, eng_obj,
               "-lpthread", "-ldl", "-lrt"])
+    # CPython fast path of the per-message send (csrc/mp_pyfast.c)
+    fast_src = os.path.join(CSRC, "mp_pyfast.c")
+    if force or _stale(FAST, [fast_src, LIB, os.path.join(INCLUDE, "mpb200.h")]):
+        _run(["gcc", "-O2", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"],
+              "-I", INCLUDE, fast_src, "-o", FAST, "-L", PKG, "-l:libmpb200.so",
+              "-Wl,-rpath,$ORIGIN"])
     return LIB
 
 

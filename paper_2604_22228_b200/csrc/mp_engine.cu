@@ -943,9 +943,10 @@ void capture(mp_ctx* ctx, Entry* e) {
 std::string make_key(const void* src, void* dst, uint64_t size, int sd, int dd, const mp_config& c) {
   struct {
     uint64_t s, d, n;
-    int32_t sd, dd, g, h, m, gm, pol;
+    int32_t sd, dd, g, h, m, gm, pol, pad;  // explicit pad: every key byte is defined
   } k{(uint64_t)(uintptr_t)src, (uint64_t)(uintptr_t)dst, size, sd, dd,
-      c.num_gpu_paths, c.host_path_enabled, c.max_chunks, c.graph_mode ? 1 : 0, c.share_policy};
+      c.num_gpu_paths, c.host_path_enabled, c.max_chunks, c.graph_mode ? 1 : 0, c.share_policy, 0};
+  static_assert(sizeof k == 3 * 8 + 8 * 4, "key has no implicit padding");
   return std::string((const char*)&k, sizeof k);
 }
 

@@ -20,7 +20,7 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
-from . import _lib
+from . import _lib, _mpfast
 from ._lib import MP_COPY_TMA, MP_COPY_VEC, MP_ENGINE_CE, MP_ENGINE_SM, check, lib
 from .paths import PathConfig, _paths_from_abi
 from .pipeline import ChunkAssignment
@@ -77,6 +77,7 @@ class Engine:
         self._ctx = C.c_void_p()
         check(lib.mp_ctx_create(n, arr, C.byref(self._ctx)))
         check(lib.mp_ctx_set_topology(self._ctx, topology._handle))
+        self._ctx_addr = self._ctx.value  # for the CPython fast path (_mpfast)
 
     @classmethod
     def loopback(cls, n_logical: int = 2, device: int = 0, link_bw: float = 3.0e12,
@@ -88,6 +89,7 @@ class Engine:
 
     def close(self):
         if getattr(self, "_ctx", None):
+            self._ctx_addr = 0
             lib.mp_ctx_destroy(self._ctx)
             self._ctx = None
 
@@ -103,6 +105,7 @@ class Engine:
     # -- configuration ------------------------------------------------------
     def set_topology(self, topology: Topology):
         check(lib.mp_ctx_set_topology(self._ctx, topology._handle))
+        self._ctx_addr = self._ctx.value  # for the CPython fast path (_mpfast)
         self.topology = topology
 
     def configure(self, *, direct: str | None = None, relay: str | None = None,
@@ -175,9 +178,11 @@ class Engine:
     # -- the transfer -------------------------------------------------------
     def send_ptr(self, src_ptr: int, dst_ptr: int, nbytes: int, src_dev: int, dst_dev: int,
                  config: PathConfig, stream: int = 0) -> None:
-        """Raw-pointer send through the C ABI (`mp_send`)."""
-        check(lib.mp_send(self._ctx, src_ptr, dst_ptr, nbytes, src_dev, dst_dev, config.abi_ref(),
-                          stream or None))
+        """Raw-pointer send through the C ABI (`mp_send`, via the CPython fast path)."""
+        rc = _mpfast.send(self._ctx_addr, src_ptr, dst_ptr, nbytes, src_dev, dst_dev,
+                          config.abi_addr(), stream or 0)
+        if rc:
+            check(rc)
 
     def send(self, src, dst, nbytes: int | None = None, config: PathConfig | None = None,
              stream=None, src_dev: int | None = None, dst_dev: int | None = None) -> None:
@@ -213,8 +218,10 @@ class Engine:
         if stream is None:
             stream = _torch().cuda.current_stream(sp)
         handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
-        check(lib.mp_send(self._ctx, src.data_ptr(), dst.data_ptr(), nbytes, src_dev, dst_dev,
-                          config.abi_ref(), handle or None))
+        rc = _mpfast.send(self._ctx_addr, src.data_ptr(), dst.data_ptr(), nbytes, src_dev, dst_dev,
+                          config.abi_addr(), handle or 0)
+        if rc:
+            check(rc)
 
     def send_many(self, transfers, config: PathConfig | None = None, joint: bool = False,
                   stream=None) -> None:

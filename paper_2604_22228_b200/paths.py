@@ -91,18 +91,19 @@ class PathConfig:
         if self.share_policy not in _POLICY_CODE:
             raise PlanError(f"unknown share policy {self.share_policy!r}")
 
-    def abi_ref(self):
-        """`byref` of this config's ABI struct, built once per instance (the
+    def abi_addr(self) -> int:
+        """Address of this config's ABI struct, built once per instance (the
         config is frozen) so a cached-graph send pays no struct conversion."""
-        ref = self.__dict__.get("_abi_ref")
-        if ref is None:
-            ref = C.byref(self.abi())
-            object.__setattr__(self, "_abi_ref", ref)
-        return ref
+        cached = self.__dict__.get("_abi_cached")
+        if cached is None:
+            struct = self.abi()
+            cached = (struct, C.addressof(struct))
+            object.__setattr__(self, "_abi_cached", cached)
+        return cached[1]
 
-    def __getstate__(self):  # the cached ctypes reference is not picklable
+    def __getstate__(self):  # the cached ctypes struct is not picklable
         state = dict(self.__dict__)
-        state.pop("_abi_ref", None)
+        state.pop("_abi_cached", None)
         return state
 
     def abi(self) -> _lib.mp_config:

@@ -74,3 +74,27 @@ def test_abi_version_and_error_text():
     rc = _lib.lib.mp_topology_load(b"[device]\n0 accelerator\n1 gpu\n", b"t", ctypes.byref(h))
     assert rc == _lib.MP_ERR_TOPOLOGY
     assert "only accelerator devices are declared" in _lib.last_error()
+
+
+def test_cpython_fast_send_keeps_the_abi_contract():
+    """The `_mpfast` send (the Python API's per-message call) is mp_send:
+    a null context returns MP_ERR_VALUE with the message in mp_last_error."""
+    from paper_2604_22228_b200 import PathConfig, _mpfast
+    cfg = PathConfig()
+    rc = _mpfast.send(0, 0, 0, 16, 0, 1, cfg.abi_addr(), 0)
+    assert rc == _lib.MP_ERR_VALUE
+    assert "null" in _lib.last_error()
+    import pytest
+    with pytest.raises(TypeError):
+        _mpfast.send(0, 0, 0)
+
+
+def test_path_config_abi_cache_pickles():
+    import pickle
+
+    from paper_2604_22228_b200 import PathConfig
+    cfg = PathConfig(num_gpu_paths=2, host_path_enabled=True, max_chunks=8)
+    addr = cfg.abi_addr()
+    assert addr == cfg.abi_addr()
+    back = pickle.loads(pickle.dumps(cfg))
+    assert back == cfg and back.abi_addr() != 0
