@@ -1,5 +1,7 @@
 #!/bin/bash
-# compute-sanitizer over a small multi-path workload (relays + host, TMA and VEC)
+# compute-sanitizer over a small multi-path workload: relays + host (TMA and
+# LDG/STG, CE and SM host paths), the small-message, static-TMA and dynamic
+# kernels, the forced peer path; graph and streamed mode
 mkdir -p gpurun_out
 python paper_2604_22228_b200/build.py > gpurun_out/build.log 2>&1 || exit 1
 cat > /tmp/san_work.py <<'PY'
@@ -8,23 +10,31 @@ sys.path.insert(0, os.getcwd())
 import torch
 import paper_2604_22228_b200 as mp
 text = mp.mesh_text("s", 4, 2e12, 1, 2e-6, 40e9, 1e-5, "full")
-for copy in ("tma", "vec"):
-    for host in ("ce", "sm"):
-        eng = mp.Engine(mp.load_topology(text), [0] * 4)
-        eng.configure(copy=copy, host=host)
-        n = (2 << 20) + 7
-        src = torch.randint(0, 256, (n + 5,), dtype=torch.uint8, device="cuda")[5:]
-        dst = torch.zeros(n, dtype=torch.uint8, device="cuda")
-        for graph in (False, True):
-            cfg = mp.PathConfig(num_gpu_paths=3, host_path_enabled=True, max_chunks=4, graph_mode=graph)
-            for _ in range(2):
-                eng.send(src, dst, n, cfg, src_dev=0, dst_dev=1)
-        eng.sync()
-        assert torch.equal(src, dst), (copy, host)
-        eng.close()
+MiB = 1 << 20
+# (engine options, gpu paths, host, size): relay + host tables (dynamic
+# claims, flag waits) with both dynamic kernels and both host mechanisms;
+# direct-only tables on the small-message kernel, the static TMA table and
+# the dynamic LDG/STG kernel; the forced peer launch path
+cases = [(dict(copy=copy, host=host), 3, True, 2 * MiB + 7)
+         for copy in ("tma", "vec") for host in ("ce", "sm")]
+cases += [({}, 1, False, 4096 + 3), ({}, 1, False, 3 * MiB + 5), ({}, 1, False, 24 * MiB + 9),
+          (dict(sched="dynamic"), 1, False, 24 * MiB + 9), (dict(tma_peer=-1), 2, True, 5 * MiB + 1)]
+for opts, g, host, n in cases:
+    eng = mp.Engine(mp.load_topology(text), [0] * 4)
+    eng.configure(**opts)
+    src = torch.randint(0, 256, (n + 5,), dtype=torch.uint8, device="cuda")[5:]
+    dst = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    for graph in (False, True):
+        cfg = mp.PathConfig(num_gpu_paths=g, host_path_enabled=host, max_chunks=4, graph_mode=graph)
+        for _ in range(2):
+            eng.send(src, dst, n, cfg, src_dev=0, dst_dev=1)
+    eng.sync()
+    assert torch.equal(src, dst), (opts, g, host, n)
+    print(opts, g, host, n, eng.stats().kernel, flush=True)
+    eng.close()
 print("workload ok")
 PY
 for tool in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool --kernel-name kns=transfer_kernel --print-limit 20 python /tmp/san_work.py > gpurun_out/sanitizer_$tool.log 2>&1
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san_work.py > gpurun_out/sanitizer_$tool.log 2>&1
   echo "$tool rc=$?"; tail -3 gpurun_out/sanitizer_$tool.log
 done
