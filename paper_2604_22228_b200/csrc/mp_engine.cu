@@ -361,6 +361,13 @@ void ensure_arenas(mp_ctx* ctx, const std::vector<size_t>& stage_need,
 // Host-path tiles stay small so many CTAs keep PCIe requests in flight.
 constexpr uint64_t kHostTileBytes = 64 << 10;
 
+// Rounds between a relay chunk's hop1 and hop2 tiles in one table (loopback,
+// or a relay sharing the source GPU): hop2 of round r queues after round
+// r + kHop2Delay, so the ~600 tiles in flight rarely include a hop2 tile whose
+// hop1 tiles are still being copied (measured, tools/exp_relay.py: 1 relay
+// 1759 -> 1800 GB/s, 6 relays 1384 -> 1420 GB/s vs a delay of 1).
+constexpr uint64_t kHop2Delay = 3;
+
 // Smallest tile of a static (one-tile-per-CTA) table: below this a message
 // spreads over fewer CTAs rather than into sub-4 KiB slivers.
 constexpr uint64_t kStaticMinTile = 4096;
@@ -667,8 +674,8 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
           h2.pass_count = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, t2);
           h2.flags = mpk::TILE_SRC_MUTABLE;
           h2.node = n_b;
-          // hop2 of round r is queued after hop1 of round r+1 (overlap, no stall)
-          append_tiles(tiles[rp], order(r2 + 3), (uint64_t)(uintptr_t)stage, d0 + ch.offset, ch.length,
+          // hop2 of round r is queued after round r + kHop2Delay (overlap, no stall)
+          append_tiles(tiles[rp], order(r2 + 1 + 2 * kHop2Delay), (uint64_t)(uintptr_t)stage, d0 + ch.offset, ch.length,
                        t2, h2);
         } else {
           int ev = new_event(sp);
