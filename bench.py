@@ -415,6 +415,7 @@ def run_ours(args, rank, world):
 
     # 6. lifecycle (BASELINE config 5) and the reference's CPU path
     lifecycle = None if args.quick else run_lifecycle(torch, eng, dev, stream)
+    windows = None if args.quick else run_windows(eng)
     relays = None if args.quick else run_relay_sweep(torch, dev, size, link_bw, host_bw,
                                                      hbm_peak / 2, pcie)
     cpu, ref_cpu = None, None
@@ -462,6 +463,7 @@ def run_ours(args, rank, world):
                   "kernels_per_send": st.kernels, "ce_copies_per_send": st.ce_copies,
                   "launch_us": st.launch_us},
         "lifecycle": lifecycle,
+        "windows": windows,
         "relay_sweep": relays,
         "sweep": sweep,
         "tuning_csv": tuning,
@@ -510,6 +512,30 @@ def run_sweep(torch, eng, topo_text, dev, stream):
     ce.close()
     auto.close()
     return rows, {"table_csv": table.to_csv(), "engine_policy": rules}
+
+
+def run_windows(eng):
+    """BASELINE config 2's posting windows (W = 1, 4, 16 as in the paper, 64 as
+    osu_bw): per window the W sends are posted back to back and the window
+    is timed on the device up to its completion (measure.run_bw, rows in the
+    reference's CSV schema), single path and direct + host k=8, each with its
+    speedup over BASELINE_CONFIG (single direct copy, per-call submission)."""
+    from paper_2604_22228_b200 import PathConfig
+    from paper_2604_22228_b200 import measure as M
+    sizes = [4 << 10, 64 << 10, MiB, 16 * MiB, 128 * MiB]
+    summary, csv_rows = {}, []
+    for w in (1, 4, 16, 64):
+        for name, cfg in (("single", PathConfig(1, False, 1, True)),
+                          ("multi_k8", PathConfig(1, True, 8, True))):
+            res = M.run_bw(M.BenchmarkSpec("omb_bw", sizes, window=w, iterations=5, warmup=3,
+                                           config=cfg, topology="b200_loopback"), eng)
+            csv_rows += res.to_csv().splitlines()[1:]
+            for r in res.rows:
+                if r.metric == "bandwidth":
+                    d = summary.setdefault(str(w), {}).setdefault(str(r.size), {})
+                    d[name] = r.value / 1e9
+                    d["baseline"] = r.value / r.speedup / 1e9
+    return {"gbs": summary, "csv": "\n".join([M.CSV_HEADER] + csv_rows) + "\n"}
 
 
 def run_relay_sweep(torch, dev, size, link_bw, host_bw, hbm_copy, pcie):

@@ -193,10 +193,15 @@ struct CeOp {
   int lane;        // lane stream index on that device
   void* dst;
   const void* src;
-  size_t len;
+  size_t len;      // bytes per row
   int wait_ev;     // index into the op-event list to wait on, -1 none
   int record_ev;   // index into the op-event list to record, -1 none
   uint32_t node;   // logical graph node (chunk-hop) id, for traces
+  // 2-D batch: `rows` rows of `len` bytes at pitches spitch / dpitch (one
+  // cudaMemcpy2DAsync moving several equal, evenly strided chunks), whose
+  // logical nodes are `nodes` (traces give each the op's interval)
+  size_t rows = 1, spitch = 0, dpitch = 0;
+  std::vector<uint32_t> nodes;
 };
 
 struct Program {
@@ -367,6 +372,18 @@ constexpr uint64_t kHostTileBytes = 64 << 10;
 // hop1 tiles are still being copied (measured, tools/exp_relay.py: 1 relay
 // 1759 -> 1800 GB/s, 6 relays 1384 -> 1420 GB/s vs a delay of 1).
 constexpr uint64_t kHop2Delay = 3;
+
+// cudaMemcpy2D pitches stay below the device's maximum pitch (2^31 - 1 class)
+constexpr uint64_t kMaxCopyPitch = 1ull << 30;
+
+// CE host path batching: the host chunks of a transfer move as
+// ceil(host bytes / kHostGroupBytes) (<= kHostMaxGroups) 2-D copy groups,
+// D2H of group g+1 overlapping H2D of group g.  Measured (tools/
+// exp_hostlanes.py, direct + host k=8, window 64): one group instead of 8
+// per-chunk D2H/H2D pairs lifts 16 MiB 340 -> 720 GB/s and 128 MiB 1912 ->
+// 2856; a 4-group pipeline pays off only when the host share is large.
+constexpr uint64_t kHostGroupBytes = 2 << 20;
+constexpr int kHostMaxGroups = 4;
 
 // Smallest tile of a static (one-tile-per-CTA) table: below this a message
 // spreads over fewer CTAs rather than into sub-4 KiB slivers.
@@ -625,6 +642,13 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
     }
     std::vector<int> hop2_done_ev(nc, -1);  // host WAR: event recorded after hop2 of chunk
     std::vector<int> host_chunk_of_seq;
+    struct HostRow {
+      uint64_t off, len;
+      int seq;
+      uint32_t n_a, n_b;
+      int p;
+    };
+    std::vector<HostRow> host_rows;  // CE host chunks in seq order (all resident)
     uint64_t host_base = host_cursor;
     for (int c = 0; c < nc; ++c) {
       const mp_chunk& ch = chunks[t][c];
@@ -713,6 +737,9 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
         append_tiles(tiles[dp], order(std::min<uint64_t>(r2 + 3, 3)), (uint64_t)(uintptr_t)slot,
                      d0 + ch.offset, ch.length, th,
                      h2);
+      } else if (eng[t].host_slots >= pi.count) {
+        // host-staged by copy engines, every chunk resident: batched below
+        host_rows.push_back(HostRow{ch.offset, ch.length, ch.seq, n_a, n_b, p});
       } else {  // host-staged: D2H into pinned staging, H2D out of it (copy engines)
         const int seq = ch.seq;
         const int slots = eng[t].host_slots;
@@ -726,16 +753,64 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
           slot = ctx->host_stage + host_cursor;
           host_cursor += ch.length;
         }
+        const int lane = lane_base[p];
         int ev1 = new_event(sp);
-        e->ce.push_back(CeOp{sp, lane_base[p], slot, (const uint8_t*)x.src + ch.offset, (size_t)ch.length,
+        e->ce.push_back(CeOp{sp, lane, slot, (const uint8_t*)x.src + ch.offset, (size_t)ch.length,
                              war, ev1, n_a});
         int ev2 = -1;
         if (slots < pi.count) {
           ev2 = new_event(dp);
           hop2_done_ev[c] = ev2;
         }
-        e->ce.push_back(CeOp{dp, lane_base[p] + 1, (uint8_t*)x.dst + ch.offset, slot, (size_t)ch.length,
+        e->ce.push_back(CeOp{dp, lane + 1, (uint8_t*)x.dst + ch.offset, slot, (size_t)ch.length,
                              ev1, ev2, n_b});
+      }
+    }
+    if (!host_rows.empty()) {
+      // The round-robin plan puts a path's full chunks at a constant stride
+      // (pipeline.py:68-77), so the host path's chunks are rows of a 2-D
+      // copy: split them into consecutive groups and move each group with ONE
+      // 2-D D2H into packed pinned staging and ONE 2-D H2D out of it (event
+      // handoff per group; D2H of group g+1 overlaps H2D of group g).  Rows
+      // that break the stride (the truncated last chunk) form their own group.
+      uint64_t hbytes = 0;
+      for (const HostRow& r : host_rows) hbytes += r.len;
+      const int ngroups = (int)std::max<uint64_t>(
+          1, std::min<uint64_t>({host_rows.size(), (uint64_t)kHostMaxGroups,
+                                 (hbytes + kHostGroupBytes - 1) / kHostGroupBytes}));
+      const size_t per = (host_rows.size() + ngroups - 1) / ngroups;
+      std::vector<std::vector<HostRow>> groups;
+      for (size_t i = 0; i < host_rows.size(); ++i) {
+        const HostRow& r = host_rows[i];
+        bool fresh = groups.empty() || groups.back().size() >= per;
+        if (!fresh) {
+          const auto& gv = groups.back();
+          const HostRow& f = gv.front();
+          const uint64_t stride = gv.size() >= 2 ? gv[1].off - gv[0].off : r.off - f.off;
+          fresh = r.len != f.len || r.off - gv.back().off != stride || stride < r.len ||
+                  stride > kMaxCopyPitch;
+        }
+        if (fresh) groups.emplace_back();
+        groups.back().push_back(r);
+      }
+      for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const auto& gv = groups[gi];
+        const HostRow& f = gv.front();
+        const uint64_t stride = gv.size() >= 2 ? gv[1].off - gv[0].off : f.len;
+        uint8_t* slot = ctx->host_stage + host_cursor;
+        host_cursor += f.len * gv.size();
+        const int lane = lane_base[f.p];  // one D2H / H2D stream pair: groups pipeline
+        CeOp d2h{sp, lane, slot, (const uint8_t*)x.src + f.off, (size_t)f.len, -1, new_event(sp), f.n_a};
+        CeOp h2d{dp, lane + 1, (uint8_t*)x.dst + f.off, slot, (size_t)f.len, d2h.record_ev, -1, f.n_b};
+        d2h.rows = h2d.rows = gv.size();
+        d2h.spitch = h2d.dpitch = stride;
+        d2h.dpitch = h2d.spitch = f.len;
+        for (const HostRow& r : gv) {
+          d2h.nodes.push_back(r.n_a);
+          h2d.nodes.push_back(r.n_b);
+        }
+        e->ce.push_back(d2h);
+        e->ce.push_back(h2d);
       }
     }
     for (int p = 0; p < np; ++p)  // reserve the slot ring of a WAR-reusing host path
@@ -902,7 +977,10 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr 
     CK(cudaSetDevice(P.ordinal));
     if (op.wait_ev >= 0) CK(cudaStreamWaitEvent(s, evs[op.wait_ev], 0));
     if (tr) CK(cudaEventRecord(tr->ce_ev[i].first, s));
-    CK(cudaMemcpyAsync(op.dst, op.src, op.len, cudaMemcpyDefault, s));
+    if (op.rows > 1)
+      CK(cudaMemcpy2DAsync(op.dst, op.dpitch, op.src, op.spitch, op.len, op.rows, cudaMemcpyDefault, s));
+    else
+      CK(cudaMemcpyAsync(op.dst, op.src, op.len, cudaMemcpyDefault, s));
     if (tr) CK(cudaEventRecord(tr->ce_ev[i].second, s));
     if (op.record_ev >= 0) CK(cudaEventRecord(evs[op.record_ev], s));
   }
@@ -1546,11 +1624,14 @@ int mp_send_trace(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_
       float a = 0.f, b = 0.f;
       CK(cudaEventElapsedTime(&a, tr.base_ev[op.phys], tr.ce_ev[i].first));
       CK(cudaEventElapsedTime(&b, tr.base_ev[op.phys], tr.ce_ev[i].second));
-      mp_trace_rec& r = out[op.node];
-      r.engine = MP_ENGINE_CE;
-      r.device = op.phys;
-      r.start_us = a * 1e3;
-      r.end_us = b * 1e3;
+      std::vector<uint32_t> nodes = op.nodes.empty() ? std::vector<uint32_t>{op.node} : op.nodes;
+      for (uint32_t nd : nodes) {
+        mp_trace_rec& r = out[nd];
+        r.engine = MP_ENGINE_CE;
+        r.device = op.phys;
+        r.start_us = a * 1e3;
+        r.end_us = b * 1e3;
+      }
     }
   } catch (...) {
     cleanup();

@@ -107,6 +107,7 @@ int main(int argc, char** argv) {
   if (variant && variant[0] == 'r') { o.copy_kind = MP_COPY_TMA; o.threads = 128; o.ctas_per_sm = 1; }
   if (variant && variant[0] == 'c') o.direct_engine = MP_ENGINE_CE;
   if (variant && variant[0] == 'p') o.tma_peer = -1; /* the NVLink-peer LDG/STG kernel */
+  if (variant && variant[0] == 'h') o.host_engine = MP_ENGINE_SM; /* SM host path */
   if (getenv("TILE")) o.tile_bytes = atoll(getenv("TILE"));
   if (getenv("CTAS")) o.ctas_per_sm = atoi(getenv("CTAS"));
   if (getenv("UNROLL")) o.unroll = atoi(getenv("UNROLL"));

@@ -16,3 +16,7 @@ for r in d.get("relay_sweep") or []:
     print({k: (round(v, 3) if isinstance(v, float) else v) for k, v in r.items()})
 for r in d.get("lifecycle") or []:
     print(r["bytes"], "replay", r["replay"], "stream", r["stream"])
+w = d.get("windows")
+if w:
+    for win, per in w["gbs"].items():
+        print("W", win, {int(k) >> 10: {a: round(b, 1) for a, b in v.items()} for k, v in per.items()})
