@@ -248,3 +248,19 @@ def test_kernel_choice_by_size(size, opts, kernel):
     st = _check(eng, text, size, graph=True, seed=5)
     assert kernel in st.kernel, st.kernel
     eng.close()
+
+
+@pytest.mark.parametrize("size,chunks", [(1000, 3), (3 * MiB + 17, 8), (9 * MiB, 16),
+                                         (40 * MiB + 5, 5), (40 * MiB + 5, 32)])
+@pytest.mark.parametrize("graph", [False, True])
+def test_host_path_2d_groups(size, chunks, graph):
+    """CE host path as 2-D copy groups (csrc/mp_engine.cu HostRow): a host
+    share of 1/3 gives several groups, a truncated last chunk its own group;
+    bytes and plan stay exact, and there are at most 2 copies per group."""
+    from paper_2604_22228_b200 import Engine, load_topology, mesh_text
+    text = mesh_text("loop", 2, 2.0e12, 1, 2e-6, 1.0e12, 10e-6, "full")
+    eng = Engine(load_topology(text), [0, 0])
+    st = _check(eng, text, size, host=True, chunks=chunks, graph=graph, reps=2, seed=13,
+                src_off=3, dst_off=3)
+    assert st.ce_copies <= 2 * 5
+    eng.close()
