@@ -264,3 +264,28 @@ def test_host_path_2d_groups(size, chunks, graph):
                 src_off=3, dst_off=3)
     assert st.ce_copies <= 2 * 5
     eng.close()
+
+
+@pytest.mark.parametrize("gpu_paths,host,chunks", [(1, False, 1), (1, True, 8), (2, True, 4)])
+def test_huge_message_beyond_4gib(gpu_paths, host, chunks):
+    """A 4.5 GiB + 5 message (byte counts past 32 bits; host chunk stride
+    near the 2-D copy pitch limit), compared on the device, plan = oracle."""
+    from paper_2604_22228_b200 import PathConfig
+    eng, text = _engine(3)
+    n = (9 << 29) + 5
+    src = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0",
+                        generator=torch.Generator(device="cuda:0").manual_seed(7))
+    dst = torch.bitwise_not(src)
+    cfg = PathConfig(num_gpu_paths=gpu_paths, host_path_enabled=host, max_chunks=chunks,
+                     graph_mode=True)
+    eng.send(src, dst, n, cfg, src_dev=0, dst_dev=1)
+    eng.sync()
+    assert torch.equal(src, dst)
+    t = op.parse_topology(text)
+    opaths = op.plan_paths(t, 0, 1, gpu_paths, host)
+    ochunks = op.make_chunk_plan([p["share"] for p in opaths], n, chunks)
+    _, done = eng.last_plan()
+    assert [(c.path_index, c.offset, c.length, c.seq) for c in done] == ochunks
+    del src, dst
+    eng.close()
+    torch.cuda.empty_cache()
