@@ -662,6 +662,64 @@ def run_group(args, rank, world):
     t = max(times)  # max over ranks
     grp.sync()
     value = args.steps * W * size / t / 1e9
+
+    # e2e through the public API from HOST memory: per window rank 0 copies
+    # the input message H2D from pinned memory, the group sends it W times,
+    # rank 1 reads back an int64 checksum of the delivered buffer (D2H);
+    # device time per rank, max over ranks
+    e2e_steps = max(2, args.steps // 2)
+    hsrc = hsum = None
+    if rank == 0:
+        hsrc = torch.empty(size, dtype=torch.uint8, pin_memory=True)
+        hsrc.copy_(src.cpu())
+    if rank == 1:
+        hsum = torch.empty(1, dtype=torch.int64, pin_memory=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    for _ in range(e2e_steps):
+        if rank == 0:
+            with torch.cuda.stream(stream):
+                src.copy_(hsrc, non_blocking=True)
+        for _ in range(W):
+            grp.transfer(sb, db, size, cfg, stream=stream)
+        if rank == 1:
+            with torch.cuda.stream(stream):
+                hsum.copy_(dst.sum(dtype=torch.int64).view(1), non_blocking=True)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    grp.sync()
+    e2e_times = [None] * world
+    dist.all_gather_object(e2e_times, c0.elapsed_time(c1) / 1e3)
+    e2e = e2e_steps * W * size / max(e2e_times) / 1e9
+    if rank == 1:
+        assert int(hsum) == ck, "e2e checksum differs"
+
+    # baseline only (not on the path): NCCL point-to-point send/recv of the
+    # same message GPU0 -> GPU1 over the NCCL process group
+    nccl = None
+    if dist.get_backend() == "nccl":
+        try:
+            reps = max(4, args.steps * W // 4)
+            buf = src if rank == 0 else (dst if rank == 1 else None)
+            dist.barrier()
+            n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for i in range(reps + 2):
+                if i == 2:
+                    n0.record()
+                if rank == 0:
+                    dist.send(buf, 1)
+                elif rank == 1:
+                    dist.recv(buf, 0)
+            n1.record()
+            torch.cuda.synchronize()
+            nt = [None] * world
+            dist.all_gather_object(nt, n0.elapsed_time(n1) / 1e3 if rank in (0, 1) else 0.0)
+            nccl = {"value": reps * size / max(nt) / 1e9, "unit": "GB/s",
+                    "what": "torch.distributed send/recv (NCCL p2p), rank 0 -> rank 1"}
+        except Exception as exc:  # noqa: BLE001 - reported, never fatal
+            nccl = {"unavailable": str(exc)[:200]}
     if rank == 0:
         peer_peak = 770.0  # measured peer copy per direction, B200_PROFILING.md
         print(json.dumps({
@@ -678,7 +736,12 @@ def run_group(args, rank, world):
                          "unit": "GB/s", "frac": value / peer_peak, "traffic": None,
                          "peak_kind": "B200_PROFILING.md measured peer copy (900 nominal)",
                          "note": "every path leaves GPU0's egress and enters GPU1's ingress"},
-            "e2e": None, "gpu_launches": args.steps * W, "clocks": clk.summary(),
+            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": size,
+                    "d2h_bytes_per_step": 8, "steps": e2e_steps,
+                    "step": f"rank 0: H2D of the input from pinned memory; {W} group "
+                            "transfers; rank 1: D2H of an int64 checksum"},
+            "nccl_p2p_baseline": nccl,
+            "gpu_launches": args.steps * W, "clocks": clk.summary(),
             "cpu_baseline": None,
         }), flush=True)
     grp.close()
