@@ -544,13 +544,6 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
   }
   ensure_arenas(ctx, stage_need, flag_devs, total_chunks, host_need);
 
-  // Static schedule (MP_SCHED_AUTO): a device whose tiles never wait on a flag
-  // and never touch host memory, and whose share is <= kStaticMaxPerCta per
-  // CTA, gets ONE tile per CTA — tile bytes = its SM
-  // bytes over (grid - 2 x segments), so cutting every chunk-hop segment
-  // still yields <= grid tiles.  The kernel then runs with no claim atomics
-  // and no exit protocol (mp_kernels.cuh); every CTA streams an equal share.
-  // Devices with waits or PCIe tiles keep dynamic claims (load balance).
   // tables that touch another GPU's memory over NVLink (see launch_transfer)
   std::vector<char> peer_phys(ctx->phys.size(), 0);
   for (int t = 0; t < T; ++t) {
