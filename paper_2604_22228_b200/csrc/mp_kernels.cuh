@@ -549,33 +549,76 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
     if (threadIdx.x == 0) bulk_wait_read<0>();
   } else {
     // ---- vector LDG/STG: the whole CTA copies each claimed tile ----
-    __shared__ unsigned s_claim[2];
-    if (threadIdx.x == 0)
-      s_claim[0] = blockIdx.x < nstatic ? blockIdx.x : atomicAdd(&ctl->work, 1u) + nstatic;
-    __syncthreads();
-    unsigned w = s_claim[0];
-    unsigned parity = 1;
-    while (w < ntiles) {
-      if (threadIdx.x == 0) {
-        s_claim[parity] = all_static ? ntiles : atomicAdd(&ctl->work, 1u) + nstatic;  // prefetch
-        s_tile = tiles[w];
-        if (s_tile.wait) wait_tile_flag(s_tile, ctl);
-        trace_start(trace, s_tile.node);
+    // Control is pipelined off the copy's critical path: thread 0 loads the
+    // NEXT tile's descriptor (claimed one tile earlier) into registers before
+    // copying its share of the current tile, and the completion signal of a
+    // tile (a system-scope release, which stalls its thread until the tile's
+    // stores are visible) is issued by thread 32 (second warp) at the start of
+    // the next tile while the other warps already copy — or by thread 0 before
+    // it waits on a flag, so a CTA never holds back a signal while it waits.
+    // Two barriers per tile.
+    __shared__ Tile s_tiles[2];
+    __shared__ unsigned s_w[2];
+    const unsigned sig_tid = blockDim.x > 32 ? 32u : 0u;  // a thread of the second warp
+    unsigned c1 = ntiles;  // thread 0: claim of the tile after the next one
+    if (threadIdx.x == 0) {
+      const unsigned w0 = blockIdx.x < nstatic ? blockIdx.x
+                                               : (all_static ? ntiles : atomicAdd(&ctl->work, 1u) + nstatic);
+      s_w[0] = w0;
+      if (w0 < ntiles) {
+        s_tiles[0] = tiles[w0];
+        c1 = all_static ? ntiles : atomicAdd(&ctl->work, 1u) + nstatic;
       }
-      __syncthreads();
-      const Tile& t = s_tile;
+    }
+    __syncthreads();
+    unsigned slot = 0;
+    uint32_t* pend_sig = nullptr;  // thread 32: the previous tile's signal
+    uint64_t pend_bytes = 0;
+    uint32_t pend_node = 0;
+    bool pend = false;
+    while (s_w[slot] < ntiles) {
+      const Tile t = s_tiles[slot];
+      Tile next{};
+      unsigned wn = ntiles;
+      if (threadIdx.x == 0) {
+        wn = c1;
+        if (wn < ntiles) {
+          next = tiles[wn];  // in flight during the copy below
+          c1 = all_static ? ntiles : atomicAdd(&ctl->work, 1u) + nstatic;
+        }
+        if (t.wait) {
+          // release the previous tile BEFORE waiting: the flag may be its own
+          if (pend) {
+            trace_end(trace, pend_node);
+            if (pend_sig) signal_tile(pend_sig, pend_bytes);
+          }
+          wait_tile_flag(t, ctl);
+        }
+        trace_start(trace, t.node);
+      }
+      __syncthreads();  // B1: the tile's flag wait is done
+      if (threadIdx.x == sig_tid && pend && !t.wait) {  // deferred completion of the previous tile
+        trace_end(trace, pend_node);
+        if (pend_sig) signal_tile(pend_sig, pend_bytes);
+      }
       if (t.flags & TILE_SRC_MUTABLE)
         copy_range<UNROLL, true>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
       else
         copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
-      __syncthreads();  // every thread's stores precede the release below
       if (threadIdx.x == 0) {
-        trace_end(trace, t.node);
-        if (t.signal) signal_tile(t.signal, sig_bytes(t));
+        s_tiles[slot ^ 1u] = next;
+        s_w[slot ^ 1u] = wn;
       }
-      w = s_claim[parity];
-      parity ^= 1u;
-      __syncthreads();  // s_tile / s_claim reuse
+      __syncthreads();  // B2: every store of the tile precedes its (deferred) release
+      pend = true;
+      pend_sig = t.signal;
+      pend_bytes = sig_bytes(t);
+      pend_node = t.node;
+      slot ^= 1u;
+    }
+    if (threadIdx.x == sig_tid && pend) {
+      trace_end(trace, pend_node);
+      if (pend_sig) signal_tile(pend_sig, pend_bytes);
     }
   }
   if (threadIdx.x == 0 && !all_static) {
