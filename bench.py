@@ -441,6 +441,11 @@ def run_ours(args, rank, world):
                      "traffic_source": ncu and ncu.get("source")},
         "path_roofline": {"R_gbs": path_roofline, "frac": value / path_roofline,
                           "hbm_copy_gbs": hbm_peak / 2, "pcie_gbs": pcie, "probe": m,
+                          # loopback: a host-staged byte is read from and written to
+                          # the same HBM as a direct byte, so PCIe cannot add to an
+                          # HBM-bound copy; the physical ceiling is the HBM copy rate
+                          "R_loopback_hbm_gbs": hbm_peak / 2,
+                          "frac_loopback_hbm": value / (hbm_peak / 2),
                           "direct_bytes": direct_bytes, "host_bytes": host_bytes,
                           "host_bw_calibrated": host_bw, "link_bw": link_bw,
                           "host_engine": "sm" if eng.options()["host_engine"] == 0 else "ce",
