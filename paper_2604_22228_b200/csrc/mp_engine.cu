@@ -49,7 +49,7 @@ namespace {
   } while (0)
 
 using KernelFn = void (*)(const mpk::Tile*, unsigned, mpk::Ctl*, unsigned, unsigned, unsigned,
-                          unsigned long long*, mpk::GroupSync);
+                          unsigned long long*, mpk::GroupSync, mpk::Sched*);
 
 KernelFn pick_kernel(const mp_engine_opts& o) {
   if (o.copy_kind == MP_COPY_TMA) return mpk::transfer_kernel<1, 8>;
@@ -116,7 +116,7 @@ void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, 
                      unsigned ntiles, mpk::Ctl* ctl, unsigned nstatic,
                      unsigned long long* trace = nullptr, const mpk::GroupSync* gsync = nullptr,
                      bool peer = false, int sms = 148, const mpk::SmallTable<mpk::kSmallMaxTiles>* small = nullptr,
-                     int kind = PROG_DYNAMIC) {
+                     int kind = PROG_DYNAMIC, mpk::Sched* sched = nullptr) {
   if (kind == PROG_SMALL && small && !trace && !gsync) {
     if (ntiles <= mpk::kSmallTilesLo) {
       mpk::SmallTable<mpk::kSmallTilesLo> lo;
@@ -149,7 +149,7 @@ void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, 
   mpk::GroupSync g{};
   if (gsync) g = *gsync;
   fn<<<grid, o.threads, smem, s>>>(tiles, ntiles, ctl, (unsigned)o.tma_stages, (unsigned)o.tma_block,
-                                   nstatic, trace, g);
+                                   nstatic, trace, g, sched);
   CK(cudaGetLastError());
 }
 
@@ -206,7 +206,8 @@ struct CeOp {
 
 struct Program {
   int phys;
-  mpk::Tile* d_tiles = nullptr;
+  mpk::Tile* d_tiles = nullptr;   // tile table, followed by the program's claim counters
+  mpk::Sched* d_sched = nullptr;  // (same allocation)
   unsigned ntiles = 0;
   unsigned grid = 0;
   unsigned nstatic = 0;  // = grid when the table has no flag waits
@@ -837,9 +838,11 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
     pr.grid = (unsigned)std::min<uint64_t>(flat.size(), pr.kind == PROG_DYNAMIC ? grid_of(ph) : P.sms);
     pr.nstatic = waits ? 0u : pr.grid;
     CK(cudaSetDevice(P.ordinal));
-    CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile)));
+    CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile) + sizeof(mpk::Sched)));
+    pr.d_sched = reinterpret_cast<mpk::Sched*>(pr.d_tiles + flat.size());
     e->progs.push_back(pr);  // owned by the entry from here (freed on error)
     CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
+    CK(cudaMemset(pr.d_sched, 0, sizeof(mpk::Sched)));
     if (pr.kind == PROG_SMALL) {
       auto sm = std::make_shared<mpk::SmallTable<mpk::kSmallMaxTiles>>();
       for (size_t i = 0; i < flat.size(); ++i) {
@@ -893,7 +896,7 @@ void enqueue_group(mp_ctx* ctx, Entry* e, cudaStream_t origin) {
   if (!e->progs.empty()) {
     const Program& pr = e->progs[0];
     launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic, nullptr, &g,
-                    pr.peer, P.sms, pr.small.get(), pr.kind);
+                    pr.peer, P.sms, pr.small.get(), pr.kind, pr.d_sched);
   } else if (e->grole == 3) {
     mpk::group_recv_kernel<<<1, 32, 0, P.kstream>>>(g, ctx->group->done(ctx->group->rank), e->expected,
                                                     P.ctl);
@@ -922,7 +925,7 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr 
     if (timing) ctx->timed_phys = pr.phys;
     if (timing) CK(cudaEventRecord(S.kt0, origin));
     launch_transfer(ctx->opts, pr.grid, origin, pr.d_tiles, pr.ntiles, S.ctl, pr.nstatic, nullptr,
-                    nullptr, pr.peer, S.sms, pr.small.get(), pr.kind);
+                    nullptr, pr.peer, S.sms, pr.small.get(), pr.kind, pr.d_sched);
     if (timing) CK(cudaEventRecord(S.kt1, origin));
     return;
   }
@@ -956,7 +959,7 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr 
     if (t) ctx->timed_phys = pr.phys;
     if (t) CK(cudaEventRecord(P.kt0, P.kstream));
     launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic,
-                    tr ? tr->stamps[pr.phys] : nullptr, nullptr, pr.peer, P.sms, pr.small.get(), pr.kind);
+                    tr ? tr->stamps[pr.phys] : nullptr, nullptr, pr.peer, P.sms, pr.small.get(), pr.kind, pr.d_sched);
     if (t) CK(cudaEventRecord(P.kt1, P.kstream));
   }
   // copy-engine lanes
@@ -1739,11 +1742,11 @@ int mp_kernel_bench(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int3
   CK(cudaSetDevice(S.ordinal));
   CK(cudaDeviceSynchronize());
   launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
-                  nullptr, pr->peer, S.sms, pr->small.get(), pr->kind);  // warm
+                  nullptr, pr->peer, S.sms, pr->small.get(), pr->kind, pr->d_sched);  // warm
   CK(cudaEventRecord(S.kt0, S.kstream));
   for (int i = 0; i < reps; ++i)
     launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
-                    nullptr, pr->peer, S.sms, pr->small.get(), pr->kind);
+                    nullptr, pr->peer, S.sms, pr->small.get(), pr->kind, pr->d_sched);
   CK(cudaEventRecord(S.kt1, S.kstream));
   CK(cudaEventSynchronize(S.kt1));
   float ms = 0.f;

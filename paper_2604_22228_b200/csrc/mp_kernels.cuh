@@ -50,6 +50,18 @@ struct GroupSync {
   int n;
 };
 
+// Claim counters of one cached program (stored right after its tile table).
+// Launch L of the program claims from work[L & 1]; L = (arrival ticket) /
+// gridDim.x because every launch of a program has the same grid and launches
+// are stream-ordered.  The first CTA of launch L zeroes work[(L + 1) & 1] for
+// the next launch (the previous user of that slot, launch L-1, has finished),
+// so dynamic tables need no exit protocol (fence + atomic per CTA + a reset
+// by the last CTA) to be replayable.
+struct __align__(16) Sched {
+  unsigned long long arrive;
+  unsigned int work[2];
+};
+
 struct __align__(16) Ctl {
   unsigned int work;     // next tile to claim
   unsigned int exit;     // CTAs finished
@@ -356,8 +368,9 @@ struct TmaEngine {
   Tile ahead;
   unsigned claim2;
   unsigned nstatic;  // tiles [0, nstatic) go to CTA blockIdx.x without a claim
+  unsigned* ctr;  // this launch's claim counter (thread 0)
   __device__ unsigned claim() {
-    return nstatic >= ntiles ? ntiles : atomicAdd(&ctl->work, 1u) + nstatic;
+    return nstatic >= ntiles ? ntiles : atomicAdd(ctr, 1u) + nstatic;
   }
   __device__ void prime() {
     next_claim = blockIdx.x < nstatic ? blockIdx.x : claim();
@@ -502,13 +515,23 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
                                                        unsigned stages, unsigned block,
                                                        unsigned nstatic,
                                                        unsigned long long* trace,
-                                                       GroupSync gsync) {
+                                                       GroupSync gsync, Sched* sched) {
   // Tiles [0, nstatic) (a prefix with no flag waits, nstatic <= gridDim.x) are
   // taken by CTA blockIdx.x without a claim; the rest are claimed dynamically.
   // A fully static table (nstatic == ntiles: one tile per CTA, no waits) runs
   // with no atomics and no exit protocol at all: the control block is
   // untouched, so a small message costs one launch and one copy.
   const bool all_static = nstatic >= ntiles && gsync.n == 0;
+  // per-program counters (no exit protocol) unless a group barrier needs the
+  // last CTA anyway; thread 0 takes its arrival ticket here
+  const bool use_sched = sched != nullptr && gsync.n == 0 && !all_static;
+  unsigned* ctr = &ctl->work;
+  if (threadIdx.x == 0 && use_sched) {
+    const unsigned long long a = atomicAdd(&sched->arrive, 1ull);
+    const unsigned long long launch = a / gridDim.x;
+    if (a % gridDim.x == 0) sched->work[(launch + 1) & 1] = 0u;
+    ctr = &sched->work[launch & 1];
+  }
   __shared__ Tile s_tile;
   __shared__ int s_cmd;
   __shared__ uint64_t s_bar[16];
@@ -521,6 +544,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
     TmaEngine eng{TmaRing{s_ring, s_bar, 0u, stages, block}, s_meta, tiles, ntiles, ctl, 0u,
                   trace};
     eng.nstatic = nstatic;
+    eng.ctr = ctr;
     if (threadIdx.x == 0) {
       for (unsigned s = 0; s < stages; ++s) mbar_init(&s_bar[s], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -563,11 +587,11 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
     unsigned c1 = ntiles;  // thread 0: claim of the tile after the next one
     if (threadIdx.x == 0) {
       const unsigned w0 = blockIdx.x < nstatic ? blockIdx.x
-                                               : (all_static ? ntiles : atomicAdd(&ctl->work, 1u) + nstatic);
+                                               : (all_static ? ntiles : atomicAdd(ctr, 1u) + nstatic);
       s_w[0] = w0;
       if (w0 < ntiles) {
         s_tiles[0] = tiles[w0];
-        c1 = all_static ? ntiles : atomicAdd(&ctl->work, 1u) + nstatic;
+        c1 = all_static ? ntiles : atomicAdd(ctr, 1u) + nstatic;
       }
     }
     __syncthreads();
@@ -584,7 +608,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
         wn = c1;
         if (wn < ntiles) {
           next = tiles[wn];  // in flight during the copy below
-          c1 = all_static ? ntiles : atomicAdd(&ctl->work, 1u) + nstatic;
+          c1 = all_static ? ntiles : atomicAdd(ctr, 1u) + nstatic;
         }
         if (t.wait) {
           // release the previous tile BEFORE waiting: the flag may be its own
@@ -621,7 +645,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       if (pend_sig) signal_tile(pend_sig, pend_bytes);
     }
   }
-  if (threadIdx.x == 0 && !all_static) {
+  if (threadIdx.x == 0 && !all_static && !use_sched) {
     __threadfence();
     if (atomicAdd(&ctl->exit, 1u) + 1u == gridDim.x) {  // last CTA re-arms the counters
       ctl->work = 0u;

@@ -127,13 +127,13 @@ int main() {
     cudaMemcpy(dt, tv.data(), tv.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice);
     unsigned nt = (unsigned)tv.size();
     printf("tma %8u B %3u tiles       %.3f us\n", bytes, nt, per_launch_us(s, [&] {
-             k_tma<<<nt, 128, 4 * 32768, s>>>(dt, nt, ctl, 4, 32768, nt, nullptr, gs);
+             k_tma<<<nt, 128, 4 * 32768, s>>>(dt, nt, ctl, 4, 32768, nt, nullptr, gs, nullptr);
            }));
     printf("tma %8u B %3u tiles, 2 stages x 16K %.3f us\n", bytes, nt, per_launch_us(s, [&] {
-             k_tma<<<nt, 128, 2 * 16384, s>>>(dt, nt, ctl, 2, 16384, nt, nullptr, gs);
+             k_tma<<<nt, 128, 2 * 16384, s>>>(dt, nt, ctl, 2, 16384, nt, nullptr, gs, nullptr);
            }));
     printf("vec %8u B %3u tiles       %.3f us\n", bytes, nt, per_launch_us(s, [&] {
-             k_vec<<<nt, 256, 0, s>>>(dt, nt, ctl, 4, 32768, nt, nullptr, gs);
+             k_vec<<<nt, 256, 0, s>>>(dt, nt, ctl, 4, 32768, nt, nullptr, gs, nullptr);
            }));
     {
       static mpk::SmallTable<mpk::kSmallMaxTiles> st;
@@ -146,7 +146,7 @@ int main() {
              per_launch_us(s, [&] { mpk::small_copy_kernel<4, mpk::kSmallMaxTiles><<<nt, 256, 0, s>>>(st); }));
     }
     printf("tma %8u B ntiles=0        %.3f us\n", bytes, per_launch_us(s, [&] {
-             k_tma<<<nt, 128, 4 * 32768, s>>>(dt, 0, ctl, 4, 32768, 0, nullptr, gs);
+             k_tma<<<nt, 128, 4 * 32768, s>>>(dt, 0, ctl, 4, 32768, 0, nullptr, gs, nullptr);
            }));
     cudaFree(dt);
   }
