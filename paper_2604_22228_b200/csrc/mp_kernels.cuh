@@ -509,6 +509,9 @@ __global__ void __launch_bounds__(256) small_copy_kernel(const __grid_constant__
 // Time base of a traced send: %globaltimer at the fork point of this device.
 __global__ void stamp_kernel(unsigned long long* out) { *out = globaltimer(); }
 
+// (LDG/STG at 4 CTAs x 256 threads per SM: 76 registers, 3 CTAs resident,
+// the 4th wave claims what is left.  Forcing 4 resident CTAs (64 registers,
+// spills) measured 174 vs 161 us at 512 MiB.)
 template <int KIND, int UNROLL>
 __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ tiles,
                                                        unsigned ntiles, Ctl* ctl,
