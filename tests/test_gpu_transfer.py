@@ -289,3 +289,27 @@ def test_huge_message_beyond_4gib(gpu_paths, host, chunks):
     del src, dst
     eng.close()
     torch.cuda.empty_cache()
+
+
+def test_kernel_timing_is_opt_in_and_errors_reraise():
+    """Streamed-mode kernel timing is off by default and on after
+    set_kernel_timing(True); ABI errors raised through the CPython fast path
+    keep the reference's exception classes and wording."""
+    from paper_2604_22228_b200 import ChunkError, PathConfig
+    from paper_2604_22228_b200._lib import EngineError
+    eng, _ = _engine(2)
+    src = torch.zeros(MiB, dtype=torch.uint8, device="cuda:0")
+    dst = torch.empty_like(src)
+    cfg = PathConfig(max_chunks=1, graph_mode=False)
+    eng.send(src, dst, MiB, cfg, src_dev=0, dst_dev=1)
+    eng.sync()
+    with pytest.raises(EngineError, match="no timed kernel"):
+        eng.kernel_time_ms()
+    eng.set_kernel_timing(True)
+    eng.send(src, dst, MiB, cfg, src_dev=0, dst_dev=1)
+    assert eng.kernel_time_ms() > 0
+    with pytest.raises(ChunkError, match="message size must be >= 1 byte"):
+        eng.send(src, dst, 0, cfg, src_dev=0, dst_dev=1)
+    eng.close()
+    with pytest.raises(ValueError, match="null"):
+        eng.send_ptr(src.data_ptr(), dst.data_ptr(), 16, 0, 1, cfg)
