@@ -456,44 +456,36 @@ struct Xfer {
   std::vector<mp_path> paths;  // pre-planned (joint planning) or empty
 };
 
-// Lower one or more transfers to device programs and copy-engine ops: ONE
-// tile table (one kernel) per physical device for every NVLink/HBM chunk-hop
-// of every transfer, interleaved round by round so concurrent transfers
-// progress together; copy-engine lanes per (transfer, path, hop).
-Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> xs,
-                         const mp_config& cfg) {
-  struct Guard {  // frees device tables of a half-built entry on error
-    mp_ctx* ctx;
-    Entry* e;
-    ~Guard() {
-      if (e) destroy_entry(ctx, e);
-    }
-    Entry* operator->() { return e; }
-    Entry* release() {
-      Entry* r = e;
-      e = nullptr;
-      return r;
-    }
-  } e{ctx, new Entry()};
-  e->key = key;
-  const mp_engine_opts& o = ctx->opts;
-  const int T = (int)xs.size();
-  if (T < 1 || T > 64) throw Error{MP_ERR_VALUE, "1..64 transfers per program"};
-  std::vector<std::vector<mp_chunk>> chunks(T);
-  std::vector<int> chunk_base(T, 0);
-  int total_chunks = 0;
-  for (int t = 0; t < T; ++t) {
-    if (xs[t].paths.empty()) xs[t].paths = plan_paths(ctx->topo, xs[t].sd, xs[t].dd, cfg);
-    chunks[t] = make_chunk_plan(xs[t].paths.data(), (int)xs[t].paths.size(), (int64_t)xs[t].size,
-                                cfg.max_chunks);
-    chunk_base[t] = total_chunks;
-    total_chunks += (int)chunks[t].size();
-    for (const mp_chunk& c : chunks[t]) e->nodes_logical += xs[t].paths[c.path_index].nhops;
+// Lowering of one or more transfers to device programs and copy-engine ops:
+// ONE tile table (one kernel) per physical device for every NVLink/HBM
+// chunk-hop of every transfer, interleaved round by round so concurrent
+// transfers progress together; copy-engine lanes per (transfer, path, hop).
+// Steps: plan (chunk plans, per-path sizes, engines, arenas) -> schedule
+// (peer tables, static vs dynamic tables) -> lower every chunk-hop -> upload.
+class Lowering {
+ public:
+  Lowering(mp_ctx* ctx, const std::string& key, std::vector<Xfer> xs)
+      : ctx_(ctx), o_(ctx->opts), xs_(std::move(xs)), e_(new Entry()) {
+    e_->key = key;
   }
-  e->paths = xs[0].paths;
-  e->chunks = chunks[0];
-  e->src_phys = ctx->logi[xs[0].sd].phys;
+  ~Lowering() {  // frees a half-built entry (and its device tables) on error
+    if (e_) destroy_entry(ctx_, e_);
+  }
+  Lowering(const Lowering&) = delete;
+  Lowering& operator=(const Lowering&) = delete;
+  Entry* build(const mp_config& cfg) {
+    plan(cfg);
+    schedule();
+    tiles_.assign(ctx_->phys.size(), {});
+    stage_cursor_.assign(ctx_->logi.size(), 0);
+    for (int t = 0; t < (int)xs_.size(); ++t) lower_transfer(t);
+    upload();
+    Entry* r = e_;
+    e_ = nullptr;
+    return r;
+  }
 
+ private:
   struct PathInfo {
     uint64_t bytes = 0, nominal = 0;
     int count = 0;
@@ -502,358 +494,431 @@ Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> 
     bool direct_sm, relay_sm, host_sm;
     int host_slots;
   };
-  std::vector<std::vector<PathInfo>> info(T);
-  std::vector<Engines> eng(T);
-  std::vector<size_t> stage_need(ctx->logi.size(), 0);
-  std::vector<char> flag_devs(ctx->logi.size(), 0);
-  size_t host_need = 0;
-  for (int t = 0; t < T; ++t) {
-    const auto& paths = xs[t].paths;
-    info[t].assign(paths.size(), PathInfo{});
-    for (const mp_chunk& c : chunks[t]) {
-      PathInfo& pi = info[t][c.path_index];
-      pi.bytes += c.length;
-      pi.nominal = std::max<uint64_t>(pi.nominal, c.length);
-      pi.count += 1;
-    }
-    // engines per path type for this message size (measured policy)
-    const bool sm_ok = xs[t].size >= (uint64_t)o.sm_min_bytes;
-    int direct_engine = o.direct_engine, host_engine = o.host_engine;
-    for (const auto& rule : ctx->size_policy)
-      if (xs[t].size <= rule.max_bytes) {
-        direct_engine = rule.direct;
-        if (rule.host >= 0) host_engine = rule.host;
-        break;
-      }
-    eng[t] = Engines{direct_engine == MP_ENGINE_SM && sm_ok, o.relay_engine == MP_ENGINE_SM && sm_ok,
-                     host_engine == MP_ENGINE_SM && sm_ok, 0};
-    for (size_t p = 0; p < paths.size(); ++p) {
-      const PathInfo& pi = info[t][p];
-      if (paths[p].kind == MP_PATH_GPU) {
-        stage_need[paths[p].stage] += pi.bytes + 16 * (size_t)pi.count;
-        if (eng[t].relay_sm) flag_devs[paths[p].stage] = 1;
-      }
-      if (paths[p].kind == MP_PATH_HOST) {
-        // the SM host path keeps every chunk resident (its share is a few MB)
-        eng[t].host_slots = (o.host_slots > 0 && !eng[t].host_sm) ? std::min(o.host_slots, pi.count)
-                                                                   : pi.count;
-        host_need += eng[t].host_slots < pi.count ? (size_t)eng[t].host_slots * pi.nominal
-                                                  : pi.bytes + 16 * (size_t)pi.count;
-        if (eng[t].host_sm) flag_devs[xs[t].dd] = 1;
-      }
-    }
-  }
-  ensure_arenas(ctx, stage_need, flag_devs, total_chunks, host_need);
-
-  // tables that touch another GPU's memory over NVLink (see launch_transfer)
-  std::vector<char> peer_phys(ctx->phys.size(), 0);
-  for (int t = 0; t < T; ++t) {
-    const int sp = ctx->logi[xs[t].sd].phys, dp = ctx->logi[xs[t].dd].phys;
-    if (sp != dp) peer_phys[o.pull ? dp : sp] = 1;
-    for (const mp_path& P : xs[t].paths)
-      if (P.kind == MP_PATH_GPU) {
-        const int rp = ctx->logi[P.stage].phys;
-        if (rp != sp) peer_phys[sp] = 1;
-        if (rp != dp) peer_phys[rp] = 1;
-      }
-  }
-  // CTAs of a device's dynamic kernel
-  auto grid_of = [&](size_t ph) {
-    int per_sm = vec_peer(o, peer_phys[ph] != 0) ? kPeerCtasPerSm : std::max(1, o.ctas_per_sm);
-    if (o.copy_kind == MP_COPY_TMA && !vec_peer(o, peer_phys[ph] != 0))  // rings that fit one SM
-      per_sm = std::min<int>(per_sm, std::max<int>(1, (int)((227u << 10) / kernel_smem(o))));
-    return (uint64_t)ctx->phys[ph].sms * per_sm;
+  // one CE host-path chunk, batched into 2-D copies (emit_host_groups)
+  struct HostRow {
+    uint64_t off, len;
+    int seq;
+    uint32_t n_a, n_b;
+    int p;
   };
+  using TileList = std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>;
 
-  // Static schedule (MP_SCHED_AUTO): a device whose tiles never wait on a flag
-  // and never touch host memory, and whose share is <= kStaticMaxPerCta per
-  // SM, gets ONE tile per SM — tile bytes = its SM bytes over (SMs - 2 x
-  // segments), so cutting every chunk-hop segment still yields <= SMs tiles.
-  // Those kernels run with no claim atomics and no exit protocol.  Devices
-  // with waits or PCIe tiles keep dynamic claims (load balance).
-  std::vector<uint64_t> static_tile(ctx->phys.size(), 0);
-  std::vector<int> static_kind(ctx->phys.size(), PROG_DYNAMIC);
-  if (o.sched == MP_SCHED_AUTO && o.tile_bytes == 0) {
-    const size_t nph = ctx->phys.size();
+  mp_ctx* ctx_;
+  const mp_engine_opts& o_;
+  std::vector<Xfer> xs_;
+  Entry* e_;
+  std::vector<std::vector<mp_chunk>> chunks_;
+  std::vector<int> chunk_base_;
+  std::vector<std::vector<PathInfo>> info_;
+  std::vector<Engines> eng_;
+  std::vector<char> peer_phys_;
+  std::vector<uint64_t> static_tile_;
+  std::vector<int> static_kind_;
+  std::vector<TileList> tiles_;
+  std::vector<uint64_t> stage_cursor_;  // shared relay arenas
+  uint64_t host_cursor_ = 0;            // shared pinned arena
+  uint32_t node_ = 0;  // logical node id of a chunk's first hop (graph.py:97-117), global
+  int lane_next_ = 0;
+
+  int phys_of(int logical) const { return ctx_->logi[logical].phys; }
+  int new_event(int phys) {
+    e_->ev_phys.push_back(phys);
+    return (int)e_->ev_phys.size() - 1;
+  }
+
+  // Chunk plans (bit-exact planner), per-path byte counts, the measured
+  // per-size engine choice, and the relay / host / flag arenas they need.
+  void plan(const mp_config& cfg) {
+    const int T = (int)xs_.size();
+    if (T < 1 || T > 64) throw Error{MP_ERR_VALUE, "1..64 transfers per program"};
+    chunks_.resize(T);
+    chunk_base_.assign(T, 0);
+    int total_chunks = 0;
+    for (int t = 0; t < T; ++t) {
+      if (xs_[t].paths.empty()) xs_[t].paths = plan_paths(ctx_->topo, xs_[t].sd, xs_[t].dd, cfg);
+      chunks_[t] = make_chunk_plan(xs_[t].paths.data(), (int)xs_[t].paths.size(),
+                                   (int64_t)xs_[t].size, cfg.max_chunks);
+      chunk_base_[t] = total_chunks;
+      total_chunks += (int)chunks_[t].size();
+      for (const mp_chunk& c : chunks_[t]) e_->nodes_logical += xs_[t].paths[c.path_index].nhops;
+    }
+    e_->paths = xs_[0].paths;
+    e_->chunks = chunks_[0];
+    e_->src_phys = phys_of(xs_[0].sd);
+
+    info_.resize(T);
+    eng_.resize(T);
+    std::vector<size_t> stage_need(ctx_->logi.size(), 0);
+    std::vector<char> flag_devs(ctx_->logi.size(), 0);
+    size_t host_need = 0;
+    for (int t = 0; t < T; ++t) {
+      const auto& paths = xs_[t].paths;
+      info_[t].assign(paths.size(), PathInfo{});
+      for (const mp_chunk& c : chunks_[t]) {
+        PathInfo& pi = info_[t][c.path_index];
+        pi.bytes += c.length;
+        pi.nominal = std::max<uint64_t>(pi.nominal, c.length);
+        pi.count += 1;
+      }
+      // engines per path type for this message size (measured policy)
+      const bool sm_ok = xs_[t].size >= (uint64_t)o_.sm_min_bytes;
+      int direct_engine = o_.direct_engine, host_engine = o_.host_engine;
+      for (const auto& rule : ctx_->size_policy)
+        if (xs_[t].size <= rule.max_bytes) {
+          direct_engine = rule.direct;
+          if (rule.host >= 0) host_engine = rule.host;
+          break;
+        }
+      eng_[t] = Engines{direct_engine == MP_ENGINE_SM && sm_ok, o_.relay_engine == MP_ENGINE_SM && sm_ok,
+                        host_engine == MP_ENGINE_SM && sm_ok, 0};
+      for (size_t p = 0; p < paths.size(); ++p) {
+        const PathInfo& pi = info_[t][p];
+        if (paths[p].kind == MP_PATH_GPU) {
+          stage_need[paths[p].stage] += pi.bytes + 16 * (size_t)pi.count;
+          if (eng_[t].relay_sm) flag_devs[paths[p].stage] = 1;
+        }
+        if (paths[p].kind == MP_PATH_HOST) {
+          // the SM host path keeps every chunk resident (its share is a few MB)
+          eng_[t].host_slots = (o_.host_slots > 0 && !eng_[t].host_sm) ? std::min(o_.host_slots, pi.count)
+                                                                       : pi.count;
+          host_need += eng_[t].host_slots < pi.count ? (size_t)eng_[t].host_slots * pi.nominal
+                                                     : pi.bytes + 16 * (size_t)pi.count;
+          if (eng_[t].host_sm) flag_devs[xs_[t].dd] = 1;
+        }
+      }
+    }
+    ensure_arenas(ctx_, stage_need, flag_devs, total_chunks, host_need);
+  }
+
+  // CTAs of a device's dynamic kernel.
+  uint64_t grid_of(size_t ph) const {
+    const bool vp = vec_peer(o_, peer_phys_[ph] != 0);
+    int per_sm = vp ? kPeerCtasPerSm : std::max(1, o_.ctas_per_sm);
+    if (o_.copy_kind == MP_COPY_TMA && !vp)  // rings that fit one SM
+      per_sm = std::min<int>(per_sm, std::max<int>(1, (int)((227u << 10) / kernel_smem(o_))));
+    return (uint64_t)ctx_->phys[ph].sms * per_sm;
+  }
+
+  // Tile bytes of a chunk-hop executed on device `ph`.
+  uint64_t tile_for(int ph, uint64_t path_bytes) const {
+    if (static_tile_[ph]) return static_tile_[ph];
+    if (o_.tile_bytes == 0 && (o_.copy_kind == MP_COPY_VEC || vec_peer(o_, peer_phys_[ph] != 0)))
+      return kVecTileBytes;
+    return auto_tile_bytes(ctx_, path_bytes, ctx_->phys[ph].sms);
+  }
+
+  // Peer tables (tiles that touch another GPU's memory over NVLink, see
+  // launch_transfer) and the static schedule (MP_SCHED_AUTO): a device whose
+  // tiles never wait on a flag and never touch host memory, and whose share
+  // is <= kStaticMaxPerCta per SM, gets ONE tile per SM — tile bytes = its SM
+  // bytes over (SMs - 2 x segments), so cutting every chunk-hop segment still
+  // yields <= SMs tiles.  Those kernels run with no claim atomics and no exit
+  // protocol.  Devices with waits or PCIe tiles keep dynamic claims.
+  void schedule() {
+    const size_t nph = ctx_->phys.size();
+    const int T = (int)xs_.size();
+    peer_phys_.assign(nph, 0);
+    for (int t = 0; t < T; ++t) {
+      const int sp = phys_of(xs_[t].sd), dp = phys_of(xs_[t].dd);
+      if (sp != dp) peer_phys_[o_.pull ? dp : sp] = 1;
+      for (const mp_path& P : xs_[t].paths)
+        if (P.kind == MP_PATH_GPU) {
+          const int rp = phys_of(P.stage);
+          if (rp != sp) peer_phys_[sp] = 1;
+          if (rp != dp) peer_phys_[rp] = 1;
+        }
+    }
+    static_tile_.assign(nph, 0);
+    static_kind_.assign(nph, PROG_DYNAMIC);
+    if (o_.sched != MP_SCHED_AUTO || o_.tile_bytes != 0) return;
     std::vector<uint64_t> sm_bytes(nph, 0);
     std::vector<int> segs(nph, 0);
     std::vector<char> dyn(nph, 0);
     for (int t = 0; t < T; ++t) {
-      const int sp = ctx->logi[xs[t].sd].phys, dp = ctx->logi[xs[t].dd].phys;
-      for (const mp_chunk& c : chunks[t]) {
-        const mp_path& P = xs[t].paths[c.path_index];
-        if (P.kind == MP_PATH_DIRECT && eng[t].direct_sm) {
-          const int ex = o.pull ? dp : sp;
+      const int sp = phys_of(xs_[t].sd), dp = phys_of(xs_[t].dd);
+      for (const mp_chunk& c : chunks_[t]) {
+        const mp_path& P = xs_[t].paths[c.path_index];
+        if (P.kind == MP_PATH_DIRECT && eng_[t].direct_sm) {
+          const int ex = o_.pull ? dp : sp;
           sm_bytes[ex] += c.length;
           segs[ex] += 1;
-        } else if (P.kind == MP_PATH_GPU && eng[t].relay_sm) {
+        } else if (P.kind == MP_PATH_GPU && eng_[t].relay_sm) {
           sm_bytes[sp] += c.length;
           segs[sp] += 1;
-          dyn[ctx->logi[P.stage].phys] = 1;
-        } else if (P.kind == MP_PATH_HOST && eng[t].host_sm) {
+          dyn[phys_of(P.stage)] = 1;
+        } else if (P.kind == MP_PATH_HOST && eng_[t].host_sm) {
           dyn[sp] = dyn[dp] = 1;
         }
       }
     }
     for (size_t ph = 0; ph < nph; ++ph) {
-      const uint64_t grid = (uint64_t)ctx->phys[ph].sms;
+      const uint64_t grid = (uint64_t)ctx_->phys[ph].sms;
       if (dyn[ph] || segs[ph] == 0 || (uint64_t)segs[ph] * 4 > grid) continue;
-      const bool small = sm_bytes[ph] <= (uint64_t)o.small_max_bytes;
-      const bool tma = sm_bytes[ph] <= grid * kStaticMaxPerCta && tma_ok(o, peer_phys[ph] != 0);
+      const bool small = sm_bytes[ph] <= (uint64_t)o_.small_max_bytes;
+      const bool tma = sm_bytes[ph] <= grid * kStaticMaxPerCta && tma_ok(o_, peer_phys_[ph] != 0);
       if (!small && !tma) continue;
       uint64_t tb = (sm_bytes[ph] + (grid - 2 * segs[ph]) - 1) / (grid - 2 * segs[ph]);
       tb = std::max<uint64_t>(tb, kStaticMinTile);
-      static_tile[ph] = (tb + 15) & ~(uint64_t)15;
-      static_kind[ph] = small ? PROG_SMALL : PROG_STATIC_TMA;
+      static_tile_[ph] = (tb + 15) & ~(uint64_t)15;
+      static_kind_[ph] = small ? PROG_SMALL : PROG_STATIC_TMA;
     }
   }
-  auto tile_for = [&](int ph, uint64_t path_bytes) {
-    if (static_tile[ph]) return static_tile[ph];
-    if (o.tile_bytes == 0 && (o.copy_kind == MP_COPY_VEC || vec_peer(o, peer_phys[ph] != 0)))
-      return kVecTileBytes;
-    return auto_tile_bytes(ctx, path_bytes, ctx->phys[ph].sms);
-  };
 
-  std::vector<std::vector<std::pair<std::pair<uint64_t, uint64_t>, mpk::Tile>>> tiles(ctx->phys.size());
-  std::vector<uint64_t> stage_cursor(ctx->logi.size(), 0);  // shared relay arenas
-  uint64_t host_cursor = 0;                                  // shared pinned arena
-  auto new_event = [&](int phys) {
-    e->ev_phys.push_back(phys);
-    return (int)e->ev_phys.size() - 1;
-  };
-  uint32_t node = 0;  // logical node id of a chunk's first hop (graph.py:97-117), global
-  int lane_next = 0;
-  for (int t = 0; t < T; ++t) {
-    const Xfer& x = xs[t];
+  // Every chunk-hop of transfer t: tiles for the SM kernels, copy-engine ops
+  // for CE paths.  Queue position of a tile: round-robin rounds, transfers
+  // interleaved; key 0 is reserved for the SM host path's hop1 tiles, which
+  // go first so their latency-bound PCIe writes overlap the whole HBM/NVLink
+  // stream instead of forming a tail.
+  void lower_transfer(int t) {
+    const Xfer& x = xs_[t];
     const auto& paths = x.paths;
-    const int np = (int)paths.size(), nc = (int)chunks[t].size();
-    const int sp = ctx->logi[x.sd].phys, dp = ctx->logi[x.dd].phys;
-    const uint64_t s0 = (uint64_t)(uintptr_t)x.src, d0 = (uint64_t)(uintptr_t)x.dst;
+    const int np = (int)paths.size(), nc = (int)chunks_[t].size();
     std::vector<int> lane_base(np, 0);
     for (int p = 0; p < np; ++p) {
-      lane_base[p] = lane_next;
-      lane_next += paths[p].nhops;
+      lane_base[p] = lane_next_;
+      lane_next_ += paths[p].nhops;
     }
     std::vector<int> hop2_done_ev(nc, -1);  // host WAR: event recorded after hop2 of chunk
     std::vector<int> host_chunk_of_seq;
-    struct HostRow {
-      uint64_t off, len;
-      int seq;
-      uint32_t n_a, n_b;
-      int p;
-    };
     std::vector<HostRow> host_rows;  // CE host chunks in seq order (all resident)
-    uint64_t host_base = host_cursor;
+    const uint64_t host_base = host_cursor_;
     for (int c = 0; c < nc; ++c) {
-      const mp_chunk& ch = chunks[t][c];
+      const mp_chunk& ch = chunks_[t][c];
       const mp_path& P = paths[ch.path_index];
       const int p = ch.path_index;
-      const int g = chunk_base[t] + c;  // flag index, unique across the program
-      const uint64_t r2 = 2 * (uint64_t)ch.seq;
-      // queue position: round-robin rounds, transfers interleaved; slot 0 is
-      // reserved for the SM host path's hop1 tiles, which go first so their
-      // latency-bound PCIe writes overlap the whole HBM/NVLink stream instead
-      // of forming a tail
-      auto order = [&](uint64_t k) { return (k + 1) * 64 + (uint64_t)t; };
-      const uint32_t n_a = node, n_b = node + 1;
-      node += (uint32_t)P.nhops;
-      const PathInfo& pi = info[t][p];
+      const uint32_t n_a = node_, n_b = node_ + 1;
+      node_ += (uint32_t)P.nhops;
+      const PathInfo& pi = info_[t][p];
+      const Engines& en = eng_[t];
       if (P.kind == MP_PATH_DIRECT) {
-        if (eng[t].direct_sm) {
-          int exec = o.pull ? dp : sp;
-          mpk::Tile proto{};
-          proto.node = n_a;
-          append_tiles(tiles[exec], order(r2), s0 + ch.offset, d0 + ch.offset, ch.length,
-                       tile_for(exec, pi.bytes), proto);
-        } else {
-          e->ce.push_back(CeOp{sp, lane_base[p], (uint8_t*)x.dst + ch.offset,
-                               (const uint8_t*)x.src + ch.offset, (size_t)ch.length, -1, -1, n_a});
-        }
+        lower_direct(t, ch, pi, n_a, lane_base[p]);
       } else if (P.kind == MP_PATH_GPU) {
-        Logi& L = ctx->logi[P.stage];
-        const int rp = L.phys;
-        // staging offset congruent to the source mod 16 keeps hop1 on the TMA path
-        uint64_t& cur = stage_cursor[P.stage];
-        cur += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)L.stage + cur)) & 15u;
-        uint8_t* stage = L.stage + cur;
-        cur += ch.length;
-        if (eng[t].relay_sm) {
-          uint64_t t1 = tile_for(sp, pi.bytes);
-          uint64_t t2 = tile_for(rp, pi.bytes);  // 64 KiB on the LDG/STG kernel (+4% vs auto)
-          mpk::Tile h1{};
-          h1.signal = L.flags + g;
-          h1.node = n_a;
-          append_tiles(tiles[sp], order(r2), s0 + ch.offset, (uint64_t)(uintptr_t)stage, ch.length, t1,
-                       h1);
-          mpk::Tile h2{};
-          h2.wait = L.flags + g;
-          h2.pass = L.flags + L.flag_cap + g;
-          h2.wait_count = (uint32_t)ntiles_of((uint64_t)(uintptr_t)stage, ch.length, t1);
-          h2.pass_count = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, t2);
-          h2.flags = mpk::TILE_SRC_MUTABLE;
-          h2.node = n_b;
-          // hop2 of round r is queued after round r + kHop2Delay (overlap, no stall)
-          append_tiles(tiles[rp], order(r2 + 1 + 2 * kHop2Delay), (uint64_t)(uintptr_t)stage, d0 + ch.offset, ch.length,
-                       t2, h2);
-        } else {
-          int ev = new_event(sp);
-          e->ce.push_back(CeOp{sp, lane_base[p], stage, (const uint8_t*)x.src + ch.offset,
-                               (size_t)ch.length, -1, ev, n_a});
-          e->ce.push_back(CeOp{rp, lane_base[p] + 1, (uint8_t*)x.dst + ch.offset, stage,
-                               (size_t)ch.length, ev, -1, n_b});
-        }
-      } else if (eng[t].host_sm) {
-        // host-staged by the SM kernels: hop1 tiles (src device) bulk-store into
-        // mapped pinned memory over PCIe, hop2 tiles (dst device) bulk-load it
-        // back after the chunk's flag (in dst memory) counts every hop1 tile.
-        Logi& L = ctx->logi[x.dd];
-        uint8_t* host_dev = nullptr;
-        CK(cudaHostGetDevicePointer((void**)&host_dev, ctx->host_stage, 0));
-        host_cursor += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)host_dev + host_cursor)) & 15u;
-        uint8_t* slot = host_dev + host_cursor;
-        host_cursor += ch.length;
-        const uint64_t th = std::min<uint64_t>(auto_tile_bytes(ctx, pi.bytes, ctx->phys[sp].sms),
-                                               kHostTileBytes);
-        mpk::Tile h1{};
-        h1.signal = L.flags + g;
-        h1.node = n_a;
-        append_tiles(tiles[sp], (uint64_t)t, s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
-        mpk::Tile h2{};
-        h2.wait = L.flags + g;
-        h2.pass = L.flags + L.flag_cap + g;
-        h2.wait_count = (uint32_t)ntiles_of((uint64_t)(uintptr_t)slot, ch.length, th);
-        h2.pass_count = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, th);
-        h2.flags = mpk::TILE_SRC_MUTABLE;
-        h2.node = n_b;
-        // every hop2 tile queues after the first two rounds: its hop1 tiles were
-        // front-loaded, so it rarely waits, and no PCIe-latency tile is left
-        // for the tail of the HBM/NVLink stream
-        append_tiles(tiles[dp], order(std::min<uint64_t>(r2 + 3, 3)), (uint64_t)(uintptr_t)slot,
-                     d0 + ch.offset, ch.length, th,
-                     h2);
-      } else if (eng[t].host_slots >= pi.count) {
-        // host-staged by copy engines, every chunk resident: batched below
-        host_rows.push_back(HostRow{ch.offset, ch.length, ch.seq, n_a, n_b, p});
-      } else {  // host-staged: D2H into pinned staging, H2D out of it (copy engines)
-        const int seq = ch.seq;
-        const int slots = eng[t].host_slots;
-        host_chunk_of_seq.push_back(c);
-        uint8_t* slot;
-        int war = -1;
-        if (slots < pi.count) {
-          slot = ctx->host_stage + host_base + (size_t)(seq % slots) * pi.nominal;
-          if (seq >= slots) war = hop2_done_ev[host_chunk_of_seq[seq - slots]];
-        } else {
-          slot = ctx->host_stage + host_cursor;
-          host_cursor += ch.length;
-        }
-        const int lane = lane_base[p];
-        int ev1 = new_event(sp);
-        e->ce.push_back(CeOp{sp, lane, slot, (const uint8_t*)x.src + ch.offset, (size_t)ch.length,
-                             war, ev1, n_a});
-        int ev2 = -1;
-        if (slots < pi.count) {
-          ev2 = new_event(dp);
-          hop2_done_ev[c] = ev2;
-        }
-        e->ce.push_back(CeOp{dp, lane + 1, (uint8_t*)x.dst + ch.offset, slot, (size_t)ch.length,
-                             ev1, ev2, n_b});
+        lower_relay(t, c, ch, P, pi, n_a, n_b, lane_base[p]);
+      } else if (en.host_sm) {
+        lower_host_sm(t, c, ch, pi, n_a, n_b);
+      } else if (en.host_slots >= pi.count) {
+        host_rows.push_back(HostRow{ch.offset, ch.length, ch.seq, n_a, n_b, p});  // batched below
+      } else {
+        lower_host_ce_slots(t, c, ch, pi, n_a, n_b, lane_base[p], host_base, hop2_done_ev,
+                            host_chunk_of_seq);
       }
     }
-    if (!host_rows.empty()) {
-      // The round-robin plan puts a path's full chunks at a constant stride
-      // (pipeline.py:68-77), so the host path's chunks are rows of a 2-D
-      // copy: split them into consecutive groups and move each group with ONE
-      // 2-D D2H into packed pinned staging and ONE 2-D H2D out of it (event
-      // handoff per group; D2H of group g+1 overlaps H2D of group g).  Rows
-      // that break the stride (the truncated last chunk) form their own group.
-      uint64_t hbytes = 0;
-      for (const HostRow& r : host_rows) hbytes += r.len;
-      const int ngroups = (int)std::max<uint64_t>(
-          1, std::min<uint64_t>({host_rows.size(), (uint64_t)kHostMaxGroups,
-                                 (hbytes + kHostGroupBytes - 1) / kHostGroupBytes}));
-      const size_t per = (host_rows.size() + ngroups - 1) / ngroups;
-      std::vector<std::vector<HostRow>> groups;
-      for (size_t i = 0; i < host_rows.size(); ++i) {
-        const HostRow& r = host_rows[i];
-        bool fresh = groups.empty() || groups.back().size() >= per;
-        if (!fresh) {
-          const auto& gv = groups.back();
-          const HostRow& f = gv.front();
-          const uint64_t stride = gv.size() >= 2 ? gv[1].off - gv[0].off : r.off - f.off;
-          fresh = r.len != f.len || r.off - gv.back().off != stride || stride < r.len ||
-                  stride > kMaxCopyPitch;
-        }
-        if (fresh) groups.emplace_back();
-        groups.back().push_back(r);
-      }
-      for (size_t gi = 0; gi < groups.size(); ++gi) {
-        const auto& gv = groups[gi];
-        const HostRow& f = gv.front();
-        const uint64_t stride = gv.size() >= 2 ? gv[1].off - gv[0].off : f.len;
-        uint8_t* slot = ctx->host_stage + host_cursor;
-        host_cursor += f.len * gv.size();
-        const int lane = lane_base[f.p];  // one D2H / H2D stream pair: groups pipeline
-        CeOp d2h{sp, lane, slot, (const uint8_t*)x.src + f.off, (size_t)f.len, -1, new_event(sp), f.n_a};
-        CeOp h2d{dp, lane + 1, (uint8_t*)x.dst + f.off, slot, (size_t)f.len, d2h.record_ev, -1, f.n_b};
-        d2h.rows = h2d.rows = gv.size();
-        d2h.spitch = h2d.dpitch = stride;
-        d2h.dpitch = h2d.spitch = f.len;
-        for (const HostRow& r : gv) {
-          d2h.nodes.push_back(r.n_a);
-          h2d.nodes.push_back(r.n_b);
-        }
-        e->ce.push_back(d2h);
-        e->ce.push_back(h2d);
-      }
-    }
+    if (!host_rows.empty()) emit_host_groups(t, host_rows, lane_base);
     for (int p = 0; p < np; ++p)  // reserve the slot ring of a WAR-reusing host path
-      if (paths[p].kind == MP_PATH_HOST && !eng[t].host_sm && eng[t].host_slots < info[t][p].count)
-        host_cursor = std::max<uint64_t>(host_cursor,
-                                         host_base + (uint64_t)eng[t].host_slots * info[t][p].nominal);
+      if (paths[p].kind == MP_PATH_HOST && !eng_[t].host_sm && eng_[t].host_slots < info_[t][p].count)
+        host_cursor_ = std::max<uint64_t>(host_cursor_,
+                                          host_base + (uint64_t)eng_[t].host_slots * info_[t][p].nominal);
   }
-  // upload one tile table per physical device
-  DeviceGuard dg;
-  for (size_t ph = 0; ph < tiles.size(); ++ph) {
-    auto& v = tiles[ph];
-    if (v.empty()) continue;
-    std::stable_sort(v.begin(), v.end(),
-                     [](const auto& a, const auto& b) { return a.first < b.first; });
-    std::vector<mpk::Tile> flat;
-    flat.reserve(v.size());
-    for (auto& kv : v) flat.push_back(kv.second);
-    Program pr;
-    pr.phys = (int)ph;
-    Phys& P = ctx->phys[ph];
-    bool waits = false, plain = true;
-    for (const auto& tl : flat) {
-      waits |= tl.wait != nullptr;
-      plain = plain && !tl.wait && !tl.signal && tl.flags == 0;
+
+  uint64_t order(int t, uint64_t k) const { return (k + 1) * 64 + (uint64_t)t; }
+
+  void lower_direct(int t, const mp_chunk& ch, const PathInfo& pi, uint32_t n_a, int lane) {
+    const Xfer& x = xs_[t];
+    const int sp = phys_of(x.sd), dp = phys_of(x.dd);
+    if (eng_[t].direct_sm) {
+      const int exec = o_.pull ? dp : sp;
+      mpk::Tile proto{};
+      proto.node = n_a;
+      append_tiles(tiles_[exec], order(t, 2 * (uint64_t)ch.seq), (uint64_t)(uintptr_t)x.src + ch.offset,
+                   (uint64_t)(uintptr_t)x.dst + ch.offset, ch.length, tile_for(exec, pi.bytes), proto);
+    } else {
+      e_->ce.push_back(CeOp{sp, lane, (uint8_t*)x.dst + ch.offset, (const uint8_t*)x.src + ch.offset,
+                            (size_t)ch.length, -1, -1, n_a});
     }
-    pr.peer = peer_phys[ph] != 0;
-    pr.kind = static_tile[ph] && flat.size() <= (size_t)P.sms ? static_kind[ph] : PROG_DYNAMIC;
-    if (pr.kind == PROG_SMALL && (!plain || flat.size() > mpk::kSmallMaxTiles))
-      pr.kind = tma_ok(o, pr.peer) ? PROG_STATIC_TMA : PROG_DYNAMIC;  // e.g. relay hop1 tiles
-    pr.ntiles = (unsigned)flat.size();
-    pr.grid = (unsigned)std::min<uint64_t>(flat.size(), pr.kind == PROG_DYNAMIC ? grid_of(ph) : P.sms);
-    pr.nstatic = waits ? 0u : pr.grid;
-    CK(cudaSetDevice(P.ordinal));
-    CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile) + sizeof(mpk::Sched)));
-    pr.d_sched = reinterpret_cast<mpk::Sched*>(pr.d_tiles + flat.size());
-    e->progs.push_back(pr);  // owned by the entry from here (freed on error)
-    CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
-    CK(cudaMemset(pr.d_sched, 0, sizeof(mpk::Sched)));
-    if (pr.kind == PROG_SMALL) {
-      auto sm = std::make_shared<mpk::SmallTable<mpk::kSmallMaxTiles>>();
-      for (size_t i = 0; i < flat.size(); ++i) {
-        sm->src[i] = flat[i].src;
-        sm->dst[i] = flat[i].dst;
-        sm->len[i] = (uint32_t)flat[i].len;
+  }
+
+  // GPU relay: hop1 src -> relay staging, hop2 staging -> dst.  SM tables
+  // hand off through the chunk's flag in the relay's memory (hop2 of round r
+  // queued after round r + kHop2Delay); CE lanes through an event.
+  void lower_relay(int t, int c, const mp_chunk& ch, const mp_path& P, const PathInfo& pi, uint32_t n_a,
+                   uint32_t n_b, int lane) {
+    const Xfer& x = xs_[t];
+    const int sp = phys_of(x.sd);
+    const uint64_t s0 = (uint64_t)(uintptr_t)x.src, d0 = (uint64_t)(uintptr_t)x.dst;
+    Logi& L = ctx_->logi[P.stage];
+    const int rp = L.phys;
+    const int g = chunk_base_[t] + c;  // flag index, unique across the program
+    // staging offset congruent to the source mod 16 keeps hop1 on the vector paths
+    uint64_t& cur = stage_cursor_[P.stage];
+    cur += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)L.stage + cur)) & 15u;
+    uint8_t* stage = L.stage + cur;
+    cur += ch.length;
+    if (!eng_[t].relay_sm) {
+      const int ev = new_event(sp);
+      e_->ce.push_back(CeOp{sp, lane, stage, (const uint8_t*)x.src + ch.offset, (size_t)ch.length, -1, ev,
+                            n_a});
+      e_->ce.push_back(CeOp{rp, lane + 1, (uint8_t*)x.dst + ch.offset, stage, (size_t)ch.length, ev, -1,
+                            n_b});
+      return;
+    }
+    const uint64_t t1 = tile_for(sp, pi.bytes);
+    const uint64_t t2 = tile_for(rp, pi.bytes);  // 64 KiB on the LDG/STG kernel (+4% vs auto)
+    mpk::Tile h1{};
+    h1.signal = L.flags + g;
+    h1.node = n_a;
+    const uint64_t r2 = 2 * (uint64_t)ch.seq;
+    append_tiles(tiles_[sp], order(t, r2), s0 + ch.offset, (uint64_t)(uintptr_t)stage, ch.length, t1, h1);
+    mpk::Tile h2{};
+    h2.wait = L.flags + g;
+    h2.pass = L.flags + L.flag_cap + g;
+    h2.wait_count = (uint32_t)ntiles_of((uint64_t)(uintptr_t)stage, ch.length, t1);
+    h2.pass_count = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, t2);
+    h2.flags = mpk::TILE_SRC_MUTABLE;
+    h2.node = n_b;
+    append_tiles(tiles_[rp], order(t, r2 + 1 + 2 * kHop2Delay), (uint64_t)(uintptr_t)stage, d0 + ch.offset,
+                 ch.length, t2, h2);
+  }
+
+  // Host-staged by the SM kernels: hop1 tiles (src device) store into mapped
+  // pinned memory over PCIe, hop2 tiles (dst device) load it back after the
+  // chunk's flag (in dst memory) counts every hop1 tile.
+  void lower_host_sm(int t, int c, const mp_chunk& ch, const PathInfo& pi, uint32_t n_a, uint32_t n_b) {
+    const Xfer& x = xs_[t];
+    const int sp = phys_of(x.sd), dp = phys_of(x.dd);
+    const uint64_t s0 = (uint64_t)(uintptr_t)x.src, d0 = (uint64_t)(uintptr_t)x.dst;
+    const int g = chunk_base_[t] + c;
+    Logi& L = ctx_->logi[x.dd];
+    uint8_t* host_dev = nullptr;
+    CK(cudaHostGetDevicePointer((void**)&host_dev, ctx_->host_stage, 0));
+    host_cursor_ += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)host_dev + host_cursor_)) & 15u;
+    uint8_t* slot = host_dev + host_cursor_;
+    host_cursor_ += ch.length;
+    const uint64_t th = std::min<uint64_t>(auto_tile_bytes(ctx_, pi.bytes, ctx_->phys[sp].sms), kHostTileBytes);
+    mpk::Tile h1{};
+    h1.signal = L.flags + g;
+    h1.node = n_a;
+    append_tiles(tiles_[sp], (uint64_t)t, s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
+    mpk::Tile h2{};
+    h2.wait = L.flags + g;
+    h2.pass = L.flags + L.flag_cap + g;
+    h2.wait_count = (uint32_t)ntiles_of((uint64_t)(uintptr_t)slot, ch.length, th);
+    h2.pass_count = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, th);
+    h2.flags = mpk::TILE_SRC_MUTABLE;
+    h2.node = n_b;
+    // every hop2 tile queues after the first two rounds: its hop1 tiles were
+    // front-loaded, so it rarely waits, and no PCIe-latency tile is left for
+    // the tail of the HBM/NVLink stream
+    append_tiles(tiles_[dp], order(t, std::min<uint64_t>(2 * (uint64_t)ch.seq + 3, 3)),
+                 (uint64_t)(uintptr_t)slot, d0 + ch.offset, ch.length, th, h2);
+  }
+
+  // Host-staged by copy engines through `host_slots` reused staging slots:
+  // per-chunk D2H then H2D (event), slot reuse guarded by a WAR event.
+  void lower_host_ce_slots(int t, int c, const mp_chunk& ch, const PathInfo& pi, uint32_t n_a,
+                           uint32_t n_b, int lane, uint64_t host_base, std::vector<int>& hop2_done_ev,
+                           std::vector<int>& host_chunk_of_seq) {
+    const Xfer& x = xs_[t];
+    const int sp = phys_of(x.sd), dp = phys_of(x.dd);
+    const int seq = ch.seq;
+    const int slots = eng_[t].host_slots;
+    host_chunk_of_seq.push_back(c);
+    uint8_t* slot = ctx_->host_stage + host_base + (size_t)(seq % slots) * pi.nominal;
+    const int war = seq >= slots ? hop2_done_ev[host_chunk_of_seq[seq - slots]] : -1;
+    const int ev1 = new_event(sp);
+    e_->ce.push_back(CeOp{sp, lane, slot, (const uint8_t*)x.src + ch.offset, (size_t)ch.length, war, ev1,
+                          n_a});
+    const int ev2 = new_event(dp);
+    hop2_done_ev[c] = ev2;
+    e_->ce.push_back(CeOp{dp, lane + 1, (uint8_t*)x.dst + ch.offset, slot, (size_t)ch.length, ev1, ev2,
+                          n_b});
+  }
+
+  // The round-robin plan puts a path's full chunks at a constant stride
+  // (pipeline.py:68-77), so the host path's chunks are rows of a 2-D copy:
+  // split them into consecutive groups and move each group with ONE 2-D D2H
+  // into packed pinned staging and ONE 2-D H2D out of it (event handoff per
+  // group; D2H of group g+1 overlaps H2D of group g).  Rows that break the
+  // stride (the truncated last chunk) form their own group.
+  void emit_host_groups(int t, const std::vector<HostRow>& host_rows, const std::vector<int>& lane_base) {
+    const Xfer& x = xs_[t];
+    const int sp = phys_of(x.sd), dp = phys_of(x.dd);
+    uint64_t hbytes = 0;
+    for (const HostRow& r : host_rows) hbytes += r.len;
+    const int ngroups = (int)std::max<uint64_t>(
+        1, std::min<uint64_t>({host_rows.size(), (uint64_t)kHostMaxGroups,
+                               (hbytes + kHostGroupBytes - 1) / kHostGroupBytes}));
+    const size_t per = (host_rows.size() + ngroups - 1) / ngroups;
+    std::vector<std::vector<HostRow>> groups;
+    for (const HostRow& r : host_rows) {
+      bool fresh = groups.empty() || groups.back().size() >= per;
+      if (!fresh) {
+        const auto& gv = groups.back();
+        const HostRow& f = gv.front();
+        const uint64_t stride = gv.size() >= 2 ? gv[1].off - gv[0].off : r.off - f.off;
+        fresh = r.len != f.len || r.off - gv.back().off != stride || stride < r.len || stride > kMaxCopyPitch;
       }
-      e->progs.back().small = sm;
+      if (fresh) groups.emplace_back();
+      groups.back().push_back(r);
+    }
+    for (const auto& gv : groups) {
+      const HostRow& f = gv.front();
+      const uint64_t stride = gv.size() >= 2 ? gv[1].off - gv[0].off : f.len;
+      uint8_t* slot = ctx_->host_stage + host_cursor_;
+      host_cursor_ += f.len * gv.size();
+      const int lane = lane_base[f.p];  // one D2H / H2D stream pair: groups pipeline
+      CeOp d2h{sp, lane, slot, (const uint8_t*)x.src + f.off, (size_t)f.len, -1, new_event(sp), f.n_a};
+      CeOp h2d{dp, lane + 1, (uint8_t*)x.dst + f.off, slot, (size_t)f.len, d2h.record_ev, -1, f.n_b};
+      d2h.rows = h2d.rows = gv.size();
+      d2h.spitch = h2d.dpitch = stride;
+      d2h.dpitch = h2d.spitch = f.len;
+      for (const HostRow& r : gv) {
+        d2h.nodes.push_back(r.n_a);
+        h2d.nodes.push_back(r.n_b);
+      }
+      e_->ce.push_back(d2h);
+      e_->ce.push_back(h2d);
     }
   }
-  return e.release();
+
+  // One tile table per physical device, sorted by queue key, its kernel kind
+  // (ProgKind), grid and static prefix, uploaded with the program's claim
+  // counters right behind it.
+  void upload() {
+    DeviceGuard dg;
+    for (size_t ph = 0; ph < tiles_.size(); ++ph) {
+      auto& v = tiles_[ph];
+      if (v.empty()) continue;
+      std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      std::vector<mpk::Tile> flat;
+      flat.reserve(v.size());
+      for (auto& kv : v) flat.push_back(kv.second);
+      Program pr;
+      pr.phys = (int)ph;
+      Phys& P = ctx_->phys[ph];
+      bool waits = false, plain = true;
+      for (const auto& tl : flat) {
+        waits |= tl.wait != nullptr;
+        plain = plain && !tl.wait && !tl.signal && tl.flags == 0;
+      }
+      pr.peer = peer_phys_[ph] != 0;
+      pr.kind = static_tile_[ph] && flat.size() <= (size_t)P.sms ? static_kind_[ph] : PROG_DYNAMIC;
+      if (pr.kind == PROG_SMALL && (!plain || flat.size() > mpk::kSmallMaxTiles))
+        pr.kind = tma_ok(o_, pr.peer) ? PROG_STATIC_TMA : PROG_DYNAMIC;  // e.g. relay hop1 tiles
+      pr.ntiles = (unsigned)flat.size();
+      pr.grid = (unsigned)std::min<uint64_t>(flat.size(), pr.kind == PROG_DYNAMIC ? grid_of(ph) : P.sms);
+      pr.nstatic = waits ? 0u : pr.grid;
+      CK(cudaSetDevice(P.ordinal));
+      CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile) + sizeof(mpk::Sched)));
+      pr.d_sched = reinterpret_cast<mpk::Sched*>(pr.d_tiles + flat.size());
+      e_->progs.push_back(pr);  // owned by the entry from here (freed on error)
+      CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
+      CK(cudaMemset(pr.d_sched, 0, sizeof(mpk::Sched)));
+      if (pr.kind == PROG_SMALL) {
+        auto sm = std::make_shared<mpk::SmallTable<mpk::kSmallMaxTiles>>();
+        for (size_t i = 0; i < flat.size(); ++i) {
+          sm->src[i] = flat[i].src;
+          sm->dst[i] = flat[i].dst;
+          sm->len[i] = (uint32_t)flat[i].len;
+        }
+        e_->progs.back().small = sm;
+      }
+    }
+  }
+};
+
+Entry* build_entry_multi(mp_ctx* ctx, const std::string& key, std::vector<Xfer> xs,
+                         const mp_config& cfg) {
+  return Lowering(ctx, key, std::move(xs)).build(cfg);
 }
 
 Entry* build_entry(mp_ctx* ctx, const std::string& key, const void* src, void* dst, uint64_t size,

@@ -109,6 +109,8 @@ int main(int argc, char** argv) {
   if (variant && variant[0] == 'p') o.tma_peer = -1; /* the NVLink-peer LDG/STG kernel */
   if (variant && variant[0] == 'h') o.host_engine = MP_ENGINE_SM; /* SM host path */
   if (getenv("TILE")) o.tile_bytes = atoll(getenv("TILE"));
+  if (getenv("STAGES")) o.tma_stages = atoi(getenv("STAGES"));
+  if (getenv("BLOCK")) o.tma_block = atoi(getenv("BLOCK"));
   if (getenv("CTAS")) o.ctas_per_sm = atoi(getenv("CTAS"));
   if (getenv("UNROLL")) o.unroll = atoi(getenv("UNROLL"));
   if (getenv("SMALL")) o.small_max_bytes = atoll(getenv("SMALL"));
