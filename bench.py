@@ -513,7 +513,7 @@ def run_sweep(torch, eng, topo_text, dev, stream):
             ("multi_stream", eng, PathConfig(1, True, 8, False)))
     for size in SWEEP_SIZES:
         src, dst = big[:size], out[:size]
-        steps = 20 if size > MiB else 100
+        steps = 20 if size > 64 * MiB else 200  # osu_bw-like steady state (64 x 100)
         warm = 3 if size > MiB else 10
         row = {"bytes": size}
         for name, e, cfg in arms:
