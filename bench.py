@@ -516,8 +516,11 @@ def run_sweep(torch, eng, topo_text, dev, stream):
         steps = 20 if size > 64 * MiB else 200  # osu_bw-like steady state (64 x 100)
         warm = 3 if size > MiB else 10
         row = {"bytes": size}
+        kernels = {}
         for name, e, cfg in arms:
             row[name] = size / time_sends(torch, e, cfg, src, dst, size, steps, warm, stream) / 1e9
+            kernels[name] = e.stats().kernel.split(" ")[0] or "copy engine"
+        row["kernels"] = kernels
         best = table.lookup(size, "graph").best
         row["tuned"] = size / time_sends(torch, auto, table.config_for(size), src, dst, size,
                                          steps, warm, stream) / 1e9
