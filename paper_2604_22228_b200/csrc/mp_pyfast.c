@@ -37,12 +37,84 @@ static PyObject* fast_send(PyObject* self, PyObject* const* args, Py_ssize_t nar
   return PyLong_FromLong(rc);
 }
 
+/* A send bound once to its arguments (Engine.prepare): calling the object
+ * replays it — one mp_send, no argument conversion at all. */
+typedef struct {
+  PyObject_HEAD
+  mp_ctx* ctx;
+  const void* src;
+  void* dst;
+  uint64_t size;
+  int32_t sd, dd;
+  const mp_config* cfg;
+  void* stream;
+  PyObject* keep; /* objects that must outlive the binding (tensors, config, stream) */
+} BoundSend;
+
+static void bound_dealloc(BoundSend* self) {
+  Py_XDECREF(self->keep);
+  Py_TYPE(self)->tp_free((PyObject*)self);
+}
+
+static PyObject* bound_call(BoundSend* self, PyObject* args, PyObject* kw) {
+  (void)args;
+  (void)kw;
+  int rc;
+  Py_BEGIN_ALLOW_THREADS
+  rc = mp_send(self->ctx, self->src, self->dst, self->size, self->sd, self->dd, self->cfg,
+               self->stream);
+  Py_END_ALLOW_THREADS
+  return PyLong_FromLong(rc);
+}
+
+static PyTypeObject BoundSendType = {
+    PyVarObject_HEAD_INIT(NULL, 0).tp_name = "_mpfast.BoundSend",
+    .tp_basicsize = sizeof(BoundSend),
+    .tp_dealloc = (destructor)bound_dealloc,
+    .tp_call = (ternaryfunc)bound_call,
+    .tp_flags = Py_TPFLAGS_DEFAULT,
+    .tp_doc = "a send bound to its arguments; call() -> MP_* status",
+};
+
+static PyObject* fast_bind(PyObject* self, PyObject* const* args, Py_ssize_t nargs) {
+  (void)self;
+  if (nargs != 9) {
+    PyErr_SetString(PyExc_TypeError, "bind(ctx, src, dst, size, src_dev, dst_dev, cfg, stream, keep)");
+    return NULL;
+  }
+  BoundSend* b = PyObject_New(BoundSend, &BoundSendType);
+  if (!b) return NULL;
+  b->keep = NULL;
+  b->ctx = (mp_ctx*)PyLong_AsVoidPtr(args[0]);
+  b->src = PyLong_AsVoidPtr(args[1]);
+  b->dst = PyLong_AsVoidPtr(args[2]);
+  b->size = (uint64_t)PyLong_AsUnsignedLongLong(args[3]);
+  long sd = PyLong_AsLong(args[4]), dd = PyLong_AsLong(args[5]);
+  b->cfg = (const mp_config*)PyLong_AsVoidPtr(args[6]);
+  b->stream = PyLong_AsVoidPtr(args[7]);
+  if (PyErr_Occurred() || sd < INT32_MIN || sd > INT32_MAX || dd < INT32_MIN || dd > INT32_MAX) {
+    if (!PyErr_Occurred()) PyErr_SetString(PyExc_OverflowError, "device index out of range");
+    Py_DECREF(b);
+    return NULL;
+  }
+  b->sd = (int32_t)sd;
+  b->dd = (int32_t)dd;
+  Py_INCREF(args[8]);
+  b->keep = args[8];
+  return (PyObject*)b;
+}
+
 static PyMethodDef methods[] = {
     {"send", (PyCFunction)(void (*)(void))fast_send, METH_FASTCALL,
      "mp_send with integer arguments; returns the MP_* status"},
+    {"bind", (PyCFunction)(void (*)(void))fast_bind, METH_FASTCALL,
+     "bind(ctx, src, dst, size, src_dev, dst_dev, cfg, stream, keep) -> BoundSend"},
     {NULL, NULL, 0, NULL}};
 
 static struct PyModuleDef module = {PyModuleDef_HEAD_INIT, "_mpfast", NULL, -1, methods,
                                     NULL, NULL, NULL, NULL};
 
-PyMODINIT_FUNC PyInit__mpfast(void) { return PyModule_Create(&module); }
+PyMODINIT_FUNC PyInit__mpfast(void) {
+  if (PyType_Ready(&BoundSendType) < 0) return NULL;
+  return PyModule_Create(&module);
+}

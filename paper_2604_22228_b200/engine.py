@@ -21,7 +21,7 @@ import ctypes as C
 from dataclasses import dataclass
 
 from . import _lib, _mpfast
-from ._lib import MP_COPY_TMA, MP_COPY_VEC, MP_ENGINE_CE, MP_ENGINE_SM, check, lib
+from ._lib import MP_COPY_TMA, MP_COPY_VEC, MP_ENGINE_CE, MP_ENGINE_SM, EngineError, check, lib
 from .paths import PathConfig, _paths_from_abi
 from .pipeline import ChunkAssignment
 from .topology import Topology, load_topology, mesh_text
@@ -184,16 +184,9 @@ class Engine:
         if rc:
             check(rc)
 
-    def send(self, src, dst, nbytes: int | None = None, config: PathConfig | None = None,
-             stream=None, src_dev: int | None = None, dst_dev: int | None = None) -> None:
-        """Move `nbytes` (default: all of `src`) from tensor `src` to tensor `dst`.
-
-        Asynchronous on `stream` (default: the current stream of src's
-        device): ordered after prior work there, and that stream waits for
-        completion.  `src_dev`/`dst_dev` are logical accelerators; by default
-        the first logical device mapped to each tensor's GPU.
-        (Kept lean: on a cached-graph hit this Python is most of the host cost.)
-        """
+    def _resolve(self, src, dst, nbytes, config, stream, src_dev, dst_dev):
+        """Validated arguments of a tensor send: (config, nbytes, src_dev,
+        dst_dev, stream handle)."""
         if config is None:
             config = PathConfig.from_env()
         sn = src.nbytes
@@ -218,10 +211,48 @@ class Engine:
         if stream is None:
             stream = _torch().cuda.current_stream(sp)
         handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        return config, nbytes, src_dev, dst_dev, handle
+
+    def send(self, src, dst, nbytes: int | None = None, config: PathConfig | None = None,
+             stream=None, src_dev: int | None = None, dst_dev: int | None = None) -> None:
+        """Move `nbytes` (default: all of `src`) from tensor `src` to tensor `dst`.
+
+        Asynchronous on `stream` (default: the current stream of src's
+        device): ordered after prior work there, and that stream waits for
+        completion.  `src_dev`/`dst_dev` are logical accelerators; by default
+        the first logical device mapped to each tensor's GPU.
+        (Kept lean: on a cached-graph hit this Python is most of the host cost.)
+        """
+        config, nbytes, src_dev, dst_dev, handle = self._resolve(src, dst, nbytes, config, stream,
+                                                                 src_dev, dst_dev)
         rc = _mpfast.send(self._ctx_addr, src.data_ptr(), dst.data_ptr(), nbytes, src_dev, dst_dev,
                           config.abi_addr(), handle or 0)
         if rc:
             check(rc)
+
+    def prepare(self, src, dst, nbytes: int | None = None, config: PathConfig | None = None,
+                stream=None, src_dev: int | None = None, dst_dev: int | None = None):
+        """Bind a send to its arguments once (same meaning as `send`) and
+        return a zero-argument callable that issues it: the per-message host
+        cost is then one C call (`_mpfast.BoundSend`), for loops that resend
+        the same buffers (osu_bw windows, halo exchanges, pipelined stages).
+        The binding keeps the tensors, config and stream alive; it must not
+        outlive the engine."""
+        config, nbytes, src_dev, dst_dev, handle = self._resolve(src, dst, nbytes, config, stream,
+                                                                 src_dev, dst_dev)
+        ctx = self._ctx_addr
+        bound = _mpfast.bind(ctx, src.data_ptr(), dst.data_ptr(), nbytes, src_dev, dst_dev,
+                             config.abi_addr(), handle or 0, (src, dst, config, stream))
+        engine = self
+
+        def launch() -> None:
+            if engine._ctx_addr != ctx:  # closed engine: never touch a freed context
+                raise EngineError("prepared send used after Engine.close()")
+            rc = bound()
+            if rc:
+                check(rc)
+        launch.bound = bound  # the raw C callable (returns the MP_* status)
+        return launch
 
     def send_many(self, transfers, config: PathConfig | None = None, joint: bool = False,
                   stream=None) -> None:

@@ -313,3 +313,25 @@ def test_kernel_timing_is_opt_in_and_errors_reraise():
     eng.close()
     with pytest.raises(ValueError, match="null"):
         eng.send_ptr(src.data_ptr(), dst.data_ptr(), 16, 0, 1, cfg)
+
+
+def test_prepared_send_replays_and_guards_close():
+    """Engine.prepare binds a send once; calling it replays the cached graph
+    (fresh bytes each time) and refuses to run after the engine is closed."""
+    from paper_2604_22228_b200 import PathConfig
+    from paper_2604_22228_b200._lib import EngineError
+    eng, _ = _engine(2)
+    n = 3 * MiB + 7
+    src = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+    dst = torch.empty_like(src)
+    go = eng.prepare(src, dst, n, PathConfig(max_chunks=4, graph_mode=True), src_dev=0, dst_dev=1)
+    for r in range(5):
+        src.copy_(torch.from_numpy(ot.pattern(n, seed=r)))
+        dst.fill_(0)
+        go()
+        eng.sync()
+        assert torch.equal(src, dst)
+    assert eng.stats().cache_hits >= 4
+    eng.close()
+    with pytest.raises(EngineError, match="after Engine.close"):
+        go()

@@ -25,8 +25,10 @@ def main():
     cfg = PathConfig(max_chunks=1, graph_mode=True)
     for n in (4096, 65536, 1 << 20):
         src, dst = big[:n], out[:n]
+        prepared = eng.prepare(src, dst, n, cfg, stream=s, src_dev=0, dst_dev=1)
         layers = {
             "send": lambda: eng.send(src, dst, n, cfg, stream=s, src_dev=0, dst_dev=1),
+            "prepare": prepared,
             "send_ptr": lambda: eng.send_ptr(src.data_ptr(), dst.data_ptr(), n, 0, 1, cfg,
                                              s.cuda_stream),
         }
