@@ -32,3 +32,36 @@ def test_reference_module_passes_against_dropin(module, tmp_path):
     probe = subprocess.run([sys.executable, "-c", "import mpsim.paths as m; print(m.__file__)"],
                            cwd=tmp_path, env=env, capture_output=True, text=True)
     assert probe.stdout.strip().startswith(os.path.join(ROOT, "paper_2604_22228_b200"))
+
+
+# The acceptance criteria that pin the hot path: 1 (byte-coverage
+# oracle over 1000 plans up to 1 GiB), 8 (node/edge counts on 500 plans) and
+# 9 (LRU over 10,000 accesses + launch-only billing on a hit).  The module
+# also imports the simulator / harness / CLI names at top level, which are
+# outside the drop-in; a pytest plugin registers inert placeholders for them
+# so the file imports — the three criteria never touch them.
+_STUB_PLUGIN = """
+import sys, types
+_NAMES = {"mpsim.bench": ["BASELINE_CONFIG", "BenchmarkSpec", "JacobiSpec", "run_bibw",
+                          "run_bw", "run_jacobi"],
+          "mpsim.cli": ["main"], "mpsim.sim": ["simulate_graph", "simulate_streamed"],
+          "mpsim.tuner": ["GridPoint", "tune"]}
+for _mod, _attrs in _NAMES.items():
+    _m = types.ModuleType(_mod)
+    for _a in _attrs:
+        setattr(_m, _a, None)
+    sys.modules[_mod] = _m
+"""
+
+
+def test_reference_acceptance_criteria_1_8_9_pass_against_dropin(tmp_path):
+    (tmp_path / "mp_outside_dropin_stubs.py").write_text(_STUB_PLUGIN)
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([str(tmp_path), COMPAT, ROOT]))
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-s", "-p", "no:cacheprovider",
+                          "-p", "mp_outside_dropin_stubs",
+                          os.path.join(REF_TESTS, "test_acceptance.py"), "--rootdir", str(tmp_path),
+                          "-k", "criterion_1_ or criterion_8 or criterion_9"],
+                         cwd=tmp_path, env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
+    for n in ("01", "08", "09"):
+        assert f"criterion {n} PASS" in res.stdout, res.stdout[-2000:]
