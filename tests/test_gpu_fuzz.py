@@ -1,8 +1,12 @@
 """Randomised GPU parity: random sizes, buffer offsets, path counts, chunk
-counts, share policies, engines and graph/streamed modes — every delivered
-byte equal to the oracle's execution of the same (oracle-checked) plan.
-Stresses the flag handoff, tile cuts, head/tail peeling and cache replays."""
+counts, share policies, engines (copy kernel, CE/SM per path type, tile
+schedule, peer launch path), cache capacities, graph/streamed modes and
+repeated sends of one entry — every delivered byte equal to the oracle's
+execution of the same (oracle-checked) plan.  Stresses the flag handoff,
+tile cuts, head/tail peeling, claim counters and cache replays/evictions.
+MP_FUZZ_ITERS sets the iteration count (default 60; soak runs use more)."""
 
+import os
 import random
 
 import numpy as np
@@ -21,18 +25,21 @@ def test_random_transfers_are_byte_exact():
     text = mp.mesh_text("fz", 5, 2.5e12, 1, 2e-6, 40e9, 1e-5, "full")
     otopo = op.parse_topology(text)
     engines = {}
-    big_src = torch.empty((24 << 20) + 64, dtype=torch.uint8, device="cuda:0")
+    big_src = torch.empty((100 << 20) + 64, dtype=torch.uint8, device="cuda:0")
     big_dst = torch.empty_like(big_src)
-    for it in range(60):
+    for it in range(int(os.environ.get("MP_FUZZ_ITERS", 60))):
         knobs = (rng.choice(["tma", "vec"]), rng.choice(["sm", "ce"]), rng.choice(["sm", "ce"]),
-                 rng.choice(["sm", "ce"]))
+                 rng.choice(["sm", "ce"]), rng.choice(["auto", "dynamic"]), rng.choice([0, -1]))
         if knobs not in engines:
             eng = mp.Engine(mp.load_topology(text), [0] * 5)
-            eng.configure(copy=knobs[0], direct=knobs[1], relay=knobs[2], host=knobs[3])
+            eng.configure(copy=knobs[0], direct=knobs[1], relay=knobs[2], host=knobs[3],
+                          sched=knobs[4], tma_peer=knobs[5])
+            if knobs[0] == "tma":
+                eng.configure(ctas_per_sm=1, threads=128)
             engines[knobs] = eng
         eng = engines[knobs]
         size = rng.choice([rng.randint(1, 4096), rng.randint(1, 1 << 20),
-                           rng.randint(1 << 20, 24 << 20)])
+                           rng.randint(1 << 20, 24 << 20), rng.randint(24 << 20, 100 << 20)])
         so, do = rng.randint(0, 63), rng.randint(0, 63)
         g = rng.randint(1, 4)
         host = rng.random() < 0.5
@@ -40,20 +47,23 @@ def test_random_transfers_are_byte_exact():
         pol = rng.choice(["equal", "bandwidth_proportional"])
         graph = rng.random() < 0.5
         cfg = mp.PathConfig(num_gpu_paths=g, host_path_enabled=host, max_chunks=k,
-                            graph_mode=graph, share_policy=pol)
-        data = ot.pattern(size, seed=it)
-        src, dst = big_src[so:so + size], big_dst[do:do + size]
-        src.copy_(torch.from_numpy(data))
-        dst.copy_(torch.bitwise_not(src))
-        eng.send(src, dst, size, cfg, src_dev=0, dst_dev=1)
-        eng.sync()
+                            graph_mode=graph, share_policy=pol,
+                            cache_capacity=rng.choice([1, 2, 16]))
         paths = op.plan_paths(otopo, 0, 1, g, host, pol)
         chunks = op.make_chunk_plan([p["share"] for p in paths], size, k)
-        _, done = eng.last_plan()
-        assert [(c.path_index, c.offset, c.length, c.seq) for c in done] == chunks
-        expect = np.empty_like(data)
-        ot.run(data, expect, [p["kind"] for p in paths], chunks, threads=4)
-        got = dst.cpu().numpy()
-        assert np.array_equal(got, expect), (it, knobs, size, so, do, g, host, k, pol, graph)
+        src, dst = big_src[so:so + size], big_dst[do:do + size]
+        for rep in range(rng.choice([1, 1, 2, 3])):  # repeats replay the cached entry
+            data = ot.pattern(size, seed=1000 * it + rep)
+            src.copy_(torch.from_numpy(data))
+            dst.copy_(torch.bitwise_not(src))
+            eng.send(src, dst, size, cfg, src_dev=0, dst_dev=1)
+            eng.sync()
+            _, done = eng.last_plan()
+            assert [(c.path_index, c.offset, c.length, c.seq) for c in done] == chunks
+            expect = np.empty_like(data)
+            ot.run(data, expect, [p["kind"] for p in paths], chunks, threads=4)
+            got = dst.cpu().numpy()
+            assert np.array_equal(got, expect), (it, rep, knobs, size, so, do, g, host, k, pol,
+                                                 graph)
     for eng in engines.values():
         eng.close()
