@@ -202,6 +202,8 @@ struct CeOp {
   // logical nodes are `nodes` (traces give each the op's interval)
   size_t rows = 1, spitch = 0, dpitch = 0;
   std::vector<uint32_t> nodes;
+  CeOp(int ph, int ln, void* d, const void* s, size_t n, int w, int r, uint32_t nd)
+      : phys(ph), lane(ln), dst(d), src(s), len(n), wait_ev(w), record_ev(r), node(nd) {}
 };
 
 struct Program {

@@ -16,6 +16,8 @@ eng = Engine(load_topology(mesh_text("b200_loopback", 2, 3.17e12, 1, 2e-6, host_
                                      "full")), [0, 0])
 if os.environ.get("HOST"):
     eng.configure(host=os.environ["HOST"])
+if os.environ.get("PROBE"):  # the bench's order: probe the paths before the buffers exist
+    eng.probe_bandwidths(256 << 20, 5, host_bytes=8 << 20)
 src = torch.randint(0, 256, (size,), dtype=torch.uint8, device="cuda")
 dst = torch.empty_like(src)
 stream = torch.cuda.Stream()
