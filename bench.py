@@ -693,33 +693,36 @@ def run_group(args, rank, world):
     # rank 1 reads back an int64 checksum of the delivered buffer (D2H);
     # device time per rank, max over ranks
     e2e_steps = max(2, args.steps // 2)
+    shared_gpu = torch.cuda.device_count() < world  # ranks time-slice one GPU (no MPS)
     hsrc = hsum = None
     if rank == 0:
         hsrc = torch.empty(size, dtype=torch.uint8, pin_memory=True)
         hsrc.copy_(src.cpu())
     if rank == 1:
         hsum = torch.empty(1, dtype=torch.int64, pin_memory=True)
-    torch.cuda.synchronize()
-    dist.barrier()
-    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    c0.record(stream)
-    for _ in range(e2e_steps):
-        if rank == 0:
-            with torch.cuda.stream(stream):
-                src.copy_(hsrc, non_blocking=True)
-        for _ in range(W):
-            grp.transfer(sb, db, size, cfg, stream=stream)
+    e2e = None
+    if not shared_gpu:
+        torch.cuda.synchronize()
+        dist.barrier()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        for _ in range(e2e_steps):
+            if rank == 0:
+                with torch.cuda.stream(stream):
+                    src.copy_(hsrc, non_blocking=True)
+            for _ in range(W):
+                grp.transfer(sb, db, size, cfg, stream=stream)
+            if rank == 1:
+                with torch.cuda.stream(stream):
+                    hsum.copy_(dst.sum(dtype=torch.int64).view(1), non_blocking=True)
+        c1.record(stream)
+        torch.cuda.synchronize()
+        grp.sync()
+        e2e_times = [None] * world
+        dist.all_gather_object(e2e_times, c0.elapsed_time(c1) / 1e3)
+        e2e = e2e_steps * W * size / max(e2e_times) / 1e9
         if rank == 1:
-            with torch.cuda.stream(stream):
-                hsum.copy_(dst.sum(dtype=torch.int64).view(1), non_blocking=True)
-    c1.record(stream)
-    torch.cuda.synchronize()
-    grp.sync()
-    e2e_times = [None] * world
-    dist.all_gather_object(e2e_times, c0.elapsed_time(c1) / 1e3)
-    e2e = e2e_steps * W * size / max(e2e_times) / 1e9
-    if rank == 1:
-        assert int(hsum) == ck, "e2e checksum differs"
+            assert int(hsum) == ck, "e2e checksum differs"
 
     # baseline only (not on the path): NCCL point-to-point send/recv of the
     # same message GPU0 -> GPU1 over the NCCL process group
@@ -761,10 +764,13 @@ def run_group(args, rank, world):
                          "unit": "GB/s", "frac": value / peer_peak, "traffic": None,
                          "peak_kind": "B200_PROFILING.md measured peer copy (900 nominal)",
                          "note": "every path leaves GPU0's egress and enters GPU1's ingress"},
-            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": size,
-                    "d2h_bytes_per_step": 8, "steps": e2e_steps,
-                    "step": f"rank 0: H2D of the input from pinned memory; {W} group "
-                            "transfers; rank 1: D2H of an int64 checksum"},
+            "e2e": ({"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": size,
+                     "d2h_bytes_per_step": 8, "steps": e2e_steps,
+                     "step": f"rank 0: H2D of the input from pinned memory; {W} group "
+                             "transfers; rank 1: D2H of an int64 checksum"}
+                    if e2e is not None else
+                    {"unavailable": "ranks share one GPU (no MPS): the e2e leg needs one GPU "
+                                    "per rank"}),
             "nccl_p2p_baseline": nccl,
             "gpu_launches": args.steps * W, "clocks": clk.summary(),
             "cpu_baseline": None,

@@ -1757,7 +1757,9 @@ int mp_sync(mp_ctx* ctx) {
     CK(cudaMemcpy(&c, P.ctl, sizeof c, cudaMemcpyDeviceToHost));
     if (c.error) {
       CK(cudaMemset(P.ctl, 0, sizeof(mpk::Ctl)));
-      return fail(MP_ERR_CUDA, "relay flag wait timed out on device " + std::to_string(P.ordinal));
+      static const char* what[] = {"", "relay flag wait", "group barrier wait", "receiver byte-count wait"};
+      return fail(MP_ERR_CUDA, std::string(c.error <= 3 ? what[c.error] : "wait") + " timed out on device " +
+                                   std::to_string(P.ordinal));
     }
   }
   return MP_OK;
