@@ -18,8 +18,15 @@ if os.environ.get("HOST"):
     eng.configure(host=os.environ["HOST"])
 if os.environ.get("PROBE"):  # the bench's order: probe the paths before the buffers exist
     eng.probe_bandwidths(256 << 20, 5, host_bytes=8 << 20)
-src = torch.randint(0, 256, (size,), dtype=torch.uint8, device="cuda")
-dst = torch.empty_like(src)
+if os.environ.get("ALLOC") == "bench":  # bench.py's allocation and fill sequence
+    src = torch.empty(size, dtype=torch.uint8, device="cuda")
+    dst = torch.empty_like(src)
+    src.copy_(torch.randint(0, 256, (size,), dtype=torch.uint8,
+                            generator=torch.Generator().manual_seed(20261017)).to(src.device))
+    dst.copy_(torch.bitwise_not(src))
+else:
+    src = torch.randint(0, 256, (size,), dtype=torch.uint8, device="cuda")
+    dst = torch.empty_like(src)
 stream = torch.cuda.Stream()
 
 
