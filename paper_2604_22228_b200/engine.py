@@ -189,6 +189,10 @@ class Engine:
         dst_dev, stream handle)."""
         if config is None:
             config = PathConfig.from_env()
+        if not (src.is_cuda and dst.is_cuda):
+            raise ValueError("send moves CUDA tensors (use torch's copies for host memory)")
+        if not (src.is_contiguous() and dst.is_contiguous()):
+            raise ValueError("send moves contiguous byte ranges: src and dst must be contiguous")
         sn = src.nbytes
         if nbytes is None:
             nbytes = sn

@@ -335,3 +335,16 @@ def test_prepared_send_replays_and_guards_close():
     eng.close()
     with pytest.raises(EngineError, match="after Engine.close"):
         go()
+
+
+def test_send_rejects_host_and_strided_tensors():
+    from paper_2604_22228_b200 import PathConfig
+    eng, _ = _engine(2)
+    cfg = PathConfig()
+    a = torch.zeros(1024, dtype=torch.uint8, device="cuda:0")
+    with pytest.raises(ValueError, match="CUDA tensors"):
+        eng.send(a.cpu(), a, 1024, cfg, src_dev=0, dst_dev=1)
+    m = torch.zeros(64, 64, dtype=torch.uint8, device="cuda:0")
+    with pytest.raises(ValueError, match="contiguous"):
+        eng.send(m.t(), torch.empty_like(m), None, cfg, src_dev=0, dst_dev=1)
+    eng.close()
