@@ -269,6 +269,8 @@ class Engine:
         arr = (_lib.mp_xfer * len(transfers))()
         first = None
         for i, (src, dst, nbytes, sd, dd) in enumerate(transfers):
+            if not (src.is_cuda and dst.is_cuda and src.is_contiguous() and dst.is_contiguous()):
+                raise ValueError("send_many moves contiguous CUDA tensors")
             n = src.numel() * src.element_size() if nbytes is None else nbytes
             if n > src.numel() * src.element_size() or n > dst.numel() * dst.element_size():
                 raise ValueError("nbytes exceeds a buffer")
