@@ -14,7 +14,7 @@ import os
 from dataclasses import dataclass, field, replace
 
 from . import _lib
-from ._lib import (MP_ERR_PLAN, MP_HOST, MP_NO_STAGE, MP_PATH_DIRECT, MP_PATH_GPU,
+from ._lib import (MP_ERR_PLAN, MP_NO_STAGE, MP_PATH_DIRECT, MP_PATH_GPU,
                    MP_PATH_HOST, MP_SHARE_BANDWIDTH, MP_SHARE_EQUAL, check, lib)
 from .topology import Channel, DeviceId, Topology, device_from_abi
 
