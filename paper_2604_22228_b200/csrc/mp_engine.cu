@@ -138,17 +138,20 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr 
       CK(cudaGetLastError());
     }
   }
-  // SM transfer kernels, one per physical device
+  // SM transfer kernels, one per physical device; the caller's device runs
+  // its kernel straight on the caller's stream (no fork/join for it)
   for (auto& pr : e->progs) {
     Phys& P = ctx->phys[pr.phys];
-    use(pr.phys, P.kstream);
+    const bool on_origin = !tr && pr.phys == e->src_phys;
+    cudaStream_t ks = on_origin ? origin : P.kstream;
+    if (!on_origin) use(pr.phys, P.kstream);
     CK(cudaSetDevice(P.ordinal));
     bool t = timing && pr.phys == e->src_phys;
     if (t) ctx->timed_phys = pr.phys;
-    if (t) CK(cudaEventRecord(P.kt0, P.kstream));
-    launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic,
+    if (t) CK(cudaEventRecord(P.kt0, ks));
+    launch_transfer(ctx->opts, pr.grid, ks, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic,
                     tr ? tr->stamps[pr.phys] : nullptr, nullptr, pr.peer, P.sms, pr.small.get(), pr.kind, pr.d_sched);
-    if (t) CK(cudaEventRecord(P.kt1, P.kstream));
+    if (t) CK(cudaEventRecord(P.kt1, ks));
   }
   // copy-engine lanes
   std::vector<cudaEvent_t> evs(e->ev_phys.size());

@@ -119,8 +119,9 @@ int main(int argc, char** argv) {
   CHECK(mp_ctx_set_engine(ctx, &o));
   const int modes = getenv("MODES") ? atoi(getenv("MODES")) : 3;
   for (int mode = 0; mode < modes; ++mode) {
-    /* 0: single path, graph replay; 1: direct + host, graph replay; 2: single path, stream */
-    mp_config cfg = {1, mode == 1, 1, mode != 2, 16, MP_SHARE_BANDWIDTH};
+    /* 0: single path, graph replay; 1: direct + host, graph replay; 2: single path,
+       stream; 3: direct + host, stream */
+    mp_config cfg = {1, mode == 1 || mode == 3, 1, mode < 2, 16, MP_SHARE_BANDWIDTH};
     for (size_t k = 0; k < sizeof sizes / sizeof sizes[0]; ++k) {
       uint64_t n = sizes[k];
       int it = n >= (128u << 20) ? iters / 100 : n >= (16u << 20) ? iters / 10 : iters;
@@ -144,7 +145,7 @@ int main(int argc, char** argv) {
       CHECK(mp_send_stats_get(ctx, &st));
       printf("{\"engine\": \"%s%s small<=%lld\", \"mode\": \"%s\", \"bytes\": %llu, \"host_us_mean\": %.3f, \"host_us_p50\": %.3f, "
              "\"host_us_p99\": %.3f, \"gpu_us_per_msg\": %.3f, \"gbs\": %.3f, \"launch_us\": %.3f}\n",
-             variant ? variant : "default", o.sched == MP_SCHED_DYNAMIC ? "+dynamic" : "", (long long)o.small_max_bytes, mode == 0 ? "single_graph" : mode == 1 ? "multi_graph" : "single_stream",
+             variant ? variant : "default", o.sched == MP_SCHED_DYNAMIC ? "+dynamic" : "", (long long)o.small_max_bytes, mode == 0 ? "single_graph" : mode == 1 ? "multi_graph" : mode == 2 ? "single_stream" : "multi_stream",
              (unsigned long long)n, sum / it, per[it / 2], per[(int)(it * 0.99)],
              ms * 1e3 / it, n / (ms * 1e-3 / it) / 1e9, st.launch_us);
       fflush(stdout);
