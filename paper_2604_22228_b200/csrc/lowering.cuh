@@ -543,8 +543,16 @@ class Lowering {
       CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile) + sizeof(mpk::Sched)));
       pr.d_sched = reinterpret_cast<mpk::Sched*>(pr.d_tiles + flat.size());
       e_->progs.push_back(pr);  // owned by the entry from here (freed on error)
-      CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
-      CK(cudaMemset(pr.d_sched, 0, sizeof(mpk::Sched)));
+      // tiles and zeroed claim counters in ONE pageable-memory cudaMemcpy,
+      // which completes before it returns: a separate cudaMemset runs on the
+      // legacy stream and is NOT ordered before a first launch on a
+      // non-blocking caller stream (it once zeroed the arrival counter under
+      // a running launch, shifting every later launch's index)
+      flat.resize(flat.size() + (sizeof(mpk::Sched) + sizeof(mpk::Tile) - 1) / sizeof(mpk::Tile));
+      std::memset(static_cast<void*>(flat.data() + pr.ntiles), 0, (flat.size() - pr.ntiles) * sizeof(mpk::Tile));
+      CK(cudaMemcpy(pr.d_tiles, flat.data(), pr.ntiles * sizeof(mpk::Tile) + sizeof(mpk::Sched),
+                    cudaMemcpyHostToDevice));
+      flat.resize(pr.ntiles);
       if (pr.kind == PROG_SMALL) {
         auto sm = std::make_shared<mpk::SmallTable<mpk::kSmallMaxTiles>>();
         for (size_t i = 0; i < flat.size(); ++i) {

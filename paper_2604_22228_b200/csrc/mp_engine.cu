@@ -475,6 +475,8 @@ int mp_ctx_create(int32_t n_logical, const int32_t* device_map, mp_ctx** out) {
     P.sms = prop.multiProcessorCount;
     CK(cudaMalloc(&P.ctl, sizeof(mpk::Ctl)));
     CK(cudaMemset(P.ctl, 0, sizeof(mpk::Ctl)));
+    CK(cudaDeviceSynchronize());  // a legacy-stream memset is not ordered before
+                                  // launches on the non-blocking caller streams
     CK(cudaStreamCreateWithFlags(&P.kstream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&P.capture, cudaStreamNonBlocking));
     CK(cudaEventCreate(&P.kt0));
@@ -881,6 +883,7 @@ int mp_sync(mp_ctx* ctx) {
     CK(cudaMemcpy(&c, P.ctl, sizeof c, cudaMemcpyDeviceToHost));
     if (c.error) {
       CK(cudaMemset(P.ctl, 0, sizeof(mpk::Ctl)));
+      CK(cudaDeviceSynchronize());
       static const char* what[] = {"", "relay flag wait", "group barrier wait", "receiver byte-count wait"};
       return fail(MP_ERR_CUDA, std::string(c.error <= 3 ? what[c.error] : "wait") + " timed out on device " +
                                    std::to_string(P.ordinal));
@@ -964,6 +967,7 @@ int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t byt
   CK(cudaSetDevice(S.ordinal));
   CK(cudaMalloc(&a, bytes));
   CK(cudaMemset(a, 1, bytes));
+  CK(cudaDeviceSynchronize());
   CK(cudaSetDevice(D.ordinal));
   CK(cudaMalloc(&b, bytes));
   CK(cudaHostAlloc((void**)&h, bytes, cudaHostAllocPortable | cudaHostAllocMapped));

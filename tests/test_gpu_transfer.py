@@ -348,3 +348,33 @@ def test_send_rejects_host_and_strided_tensors():
     with pytest.raises(ValueError, match="contiguous"):
         eng.send(m.t(), torch.empty_like(m), None, cfg, src_dev=0, dst_dev=1)
     eng.close()
+
+
+def test_streamed_dynamic_tables_match_graph_replays():
+    """Per-call (streamed) sends of a dynamic table issued back to back on a
+    non-blocking stream right after the entry is built: bytes exact, and the
+    launch-parity claim counters stay in step — a desynchronised counter
+    makes CTAs re-claim tiles (correct bytes, ~1.5x the time), so the
+    streamed rate must stay within 25% of cached-graph replays."""
+    from paper_2604_22228_b200 import PathConfig
+    eng, _ = _engine(2)
+    n = 256 * MiB
+    src = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0")
+    dst = torch.empty_like(src)
+    s = torch.cuda.Stream()
+    rates = {}
+    for graph in (False, True):
+        cfg = PathConfig(max_chunks=1, graph_mode=graph)
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                eng.send(src, dst, n, cfg, stream=s, src_dev=0, dst_dev=1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(20):
+                eng.send(src, dst, n, cfg, stream=s, src_dev=0, dst_dev=1)
+            e1.record(s)
+        torch.cuda.synchronize()
+        assert torch.equal(src, dst)
+        rates[graph] = e0.elapsed_time(e1)
+    assert rates[False] < 1.25 * rates[True], rates
+    eng.close()

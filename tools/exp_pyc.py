@@ -13,7 +13,14 @@ from paper_2604_22228_b200 import Engine, PathConfig, _lib, _mpfast  # noqa: E40
 n = int(os.environ.get("SIZE", 16 << 20))
 iters = int(os.environ.get("ITERS", 2000))
 eng = Engine.loopback(2)
-big = torch.randint(0, 256, (512 << 20,), dtype=torch.uint8, device="cuda")
+if os.environ.get("EMPTY"):  # the bench sweep's buffers: torch.empty, never written first
+    big = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    if os.environ["EMPTY"] == "zero":
+        big.zero_()
+    elif os.environ["EMPTY"] == "ones":
+        big.fill_(0xA5)
+else:
+    big = torch.randint(0, 256, (512 << 20,), dtype=torch.uint8, device="cuda")
 out = torch.empty_like(big)
 src, dst = big[:n], out[:n]
 s = torch.cuda.Stream()
@@ -57,6 +64,8 @@ addr = cfg.abi_addr()
 timed("Engine.send", lambda: eng.send(src, dst, n, cfg, stream=s, src_dev=0, dst_dev=1))
 timed("_mpfast.send", lambda: _mpfast.send(eng._ctx_addr, sp, dp, n, 0, 1, addr, h))
 ref = C.byref(cfg.abi())
+if os.environ.get("QUICK"):
+    sys.exit(0)
 timed("ctypes mp_send", lambda: _lib.lib.mp_send(eng._ctx, sp, dp, n, 0, 1, ref, h))
 # fresh cudaMalloc-like buffers (torch empty, separate allocations)
 a = torch.empty(n, dtype=torch.uint8, device="cuda")
