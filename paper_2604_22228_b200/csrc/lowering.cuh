@@ -543,11 +543,10 @@ class Lowering {
       CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile) + sizeof(mpk::Sched)));
       pr.d_sched = reinterpret_cast<mpk::Sched*>(pr.d_tiles + flat.size());
       e_->progs.push_back(pr);  // owned by the entry from here (freed on error)
-      // tiles and zeroed claim counters in ONE pageable-memory cudaMemcpy,
-      // which completes before it returns: a separate cudaMemset runs on the
-      // legacy stream and is NOT ordered before a first launch on a
-      // non-blocking caller stream (it once zeroed the arrival counter under
-      // a running launch, shifting every later launch's index)
+      // tiles and zeroed claim counters in ONE upload, completed below before
+      // any launch (an unsynchronised legacy-stream cudaMemset once zeroed
+      // the arrival counter under a running first launch on a non-blocking
+      // caller stream, shifting every later launch's index)
       flat.resize(flat.size() + (sizeof(mpk::Sched) + sizeof(mpk::Tile) - 1) / sizeof(mpk::Tile));
       std::memset(static_cast<void*>(flat.data() + pr.ntiles), 0, (flat.size() - pr.ntiles) * sizeof(mpk::Tile));
       CK(cudaMemcpy(pr.d_tiles, flat.data(), pr.ntiles * sizeof(mpk::Tile) + sizeof(mpk::Sched),
@@ -562,6 +561,13 @@ class Lowering {
         }
         e_->progs.back().small = sm;
       }
+    }
+    // A pageable-memory cudaMemcpy may return before its DMA reaches the
+    // device, and it runs on the legacy stream, which the non-blocking
+    // caller streams do not wait for: finish the uploads before any launch.
+    for (const Program& pr : e_->progs) {
+      CK(cudaSetDevice(ctx_->phys[pr.phys].ordinal));
+      CK(cudaStreamSynchronize(cudaStreamLegacy));
     }
   }
 };

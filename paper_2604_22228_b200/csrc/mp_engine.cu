@@ -379,6 +379,7 @@ Entry* build_group_entry(mp_ctx* ctx, const std::string& key, const void* src, u
     CK(cudaSetDevice(ctx->phys[0].ordinal));
     CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile)));
     CK(cudaMemcpy(pr.d_tiles, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
+    CK(cudaStreamSynchronize(cudaStreamLegacy));  // the upload lands before any launch
     e->progs.push_back(pr);
   }
   return e.release();
@@ -996,6 +997,7 @@ int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t byt
   CK(cudaSetDevice(S.ordinal));
   CK(cudaMalloc(&dt, flat.size() * sizeof(mpk::Tile)));
   CK(cudaMemcpy(dt, flat.data(), flat.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
+  CK(cudaStreamSynchronize(cudaStreamLegacy));
   unsigned grid = (unsigned)std::min<uint64_t>(flat.size(), (uint64_t)S.sms * ctx->opts.ctas_per_sm);
   out_gbps[0] = time_it(S, [&](cudaStream_t s) {
     launch_transfer(ctx->opts, grid, s, dt, (unsigned)flat.size(), S.ctl, grid);
@@ -1022,6 +1024,7 @@ int mp_measure_paths(mp_ctx* ctx, int32_t src_dev, int32_t dst_dev, uint64_t byt
       CK(cudaSetDevice(S.ordinal));
       CK(cudaMalloc(&d, ft.size() * sizeof(mpk::Tile)));
       CK(cudaMemcpy(d, ft.data(), ft.size() * sizeof(mpk::Tile), cudaMemcpyHostToDevice));
+      CK(cudaStreamSynchronize(cudaStreamLegacy));
       unsigned gr = (unsigned)std::min<uint64_t>(ft.size(), (uint64_t)S.sms * ctx->opts.ctas_per_sm);
       double r = time_it(S, [&](cudaStream_t s) {
         launch_transfer(ctx->opts, gr, s, d, (unsigned)ft.size(), S.ctl, gr);
