@@ -14,7 +14,11 @@ reference-style analysis and plots consume real B200 data:
 * `run_bibw`    — two opposite flows per window slot as one program
                   (`Engine.send_many`), aggregate bandwidth;
 * `run_latency` — single-message latency first / steady and the four
-                  lifecycle phases measured by the engine (graph.py:24).
+                  lifecycle phases measured by the engine (graph.py:24);
+* `run_jacobi`  — 4-rank ring halo exchange of a Jacobi iteration
+                  (bench.py:280-390): real forward + backward ring phases,
+                  planned jointly, against the single-path baseline, with
+                  the halo rows checked byte-exact.
 Times are seconds, bandwidths bytes/s, as in the reference.
 """
 
@@ -74,6 +78,7 @@ class BenchRow:
 @dataclass
 class BenchResult:
     rows: list[BenchRow]
+    integrity_all_clear: bool = True
 
     def to_csv(self) -> str:
         return "\n".join([CSV_HEADER] + [r.to_csv() for r in self.rows]) + "\n"
@@ -82,6 +87,14 @@ class BenchResult:
         for row in self.rows:
             if row.size == size and row.metric == metric:
                 return row.value
+        raise KeyError(f"no row for size={size} metric={metric}")
+
+    def speedup(self, size: int, metric: str) -> float:
+        for row in self.rows:
+            if row.size == size and row.metric == metric:
+                if row.speedup is None:
+                    raise KeyError(f"row size={size} metric={metric} has no speedup")
+                return row.speedup
         raise KeyError(f"no row for size={size} metric={metric}")
 
 
@@ -206,3 +219,132 @@ def run_latency(spec: BenchmarkSpec, engine, src_dev: int = 0, dst_dev: int = 1)
 
 def with_chunks(config: PathConfig, chunks: int) -> PathConfig:
     return replace(config, max_chunks=chunks)
+
+
+@dataclass
+class JacobiSpec:
+    """Problem sizes of the ring halo exchange (bench.py:280-301): rank r owns
+    `ny` rows of `nx / ranks` elements; its first and last rows travel to the
+    ring neighbours every iteration, so one halo is `nx * element_size / ranks`
+    bytes.  `timed` bounds how many steady exchanges are measured (the
+    runtime is extrapolated to `iterations` as the reference does: first +
+    steady * (iterations - 1))."""
+    nx_values: list[int]
+    ranks: int = 4
+    ny: int = 8
+    element_size: int = 8
+    iterations: int = 1000
+    compute_time_per_cell: float = 0.0
+    timed: int = 20
+
+    def __post_init__(self):
+        if self.ranks != 4:
+            raise ValueError("the halo-exchange model is defined for 4 ranks")
+        if not self.nx_values:
+            raise ValueError("no problem sizes given")
+        for nx in self.nx_values:
+            if nx % self.ranks:
+                raise ValueError(f"nx={nx} is not divisible by {self.ranks} ranks")
+        if self.element_size != 8:
+            raise ValueError("the measured exchange moves float64 rows (element_size 8)")
+        if self.timed < 1 or self.iterations < 1:
+            raise ValueError("iterations must be >= 1")
+
+    def halo_bytes(self, nx: int) -> int:
+        return nx * self.element_size // self.ranks
+
+    def compute_seconds(self, nx: int) -> float:
+        return nx * self.ny * self.compute_time_per_cell / self.ranks
+
+
+class _Ring:
+    """Rank grids `[(ny + 2) x w]` float64 (row 0 / row ny+1 = halos from the
+    previous / next rank) and the two ring phases of one exchange
+    (bench.py:311-330): forward r -> r+1 carries row ny into the next rank's
+    row 0, backward r -> r-1 carries row 1 into the previous rank's row ny+1."""
+
+    def __init__(self, engine, spec, nx, stream):
+        import torch
+        self.engine, self.stream, self.ranks = engine, stream, spec.ranks
+        w, ny = nx // spec.ranks, spec.ny
+        g = torch.Generator(device="cpu").manual_seed(20261017)
+        self.grids = [torch.rand((ny + 2, w), dtype=torch.float64, generator=g)
+                      .to(f"cuda:{engine.device_map[r]}") for r in range(spec.ranks)]
+        n, R = w * 8, spec.ranks
+        self.phases = [
+            [(self.grids[r][ny], self.grids[(r + 1) % R][0], n, r, (r + 1) % R) for r in range(R)],
+            [(self.grids[r][1], self.grids[(r - 1) % R][ny + 1], n, r, (r - 1) % R)
+             for r in range(R)],
+        ]
+
+    def compute(self):
+        """One Jacobi sweep of every rank's interior rows (5-point average,
+        edge columns held), on the exchange stream."""
+        import torch
+        with torch.cuda.stream(self.stream):
+            for g in self.grids:
+                c = g[1:-1, 1:-1]
+                c.copy_(0.25 * (g[:-2, 1:-1] + g[2:, 1:-1] + g[1:-1, :-2] + g[1:-1, 2:]))
+
+    def exchange(self, cfg):
+        joint = cfg.num_gpu_paths > 1 or cfg.host_path_enabled  # bench.py:322-325
+        for phase in self.phases:
+            self.engine.send_many(phase, cfg, joint=joint, stream=self.stream)
+
+    def halos_match(self) -> bool:
+        import torch
+        torch.cuda.synchronize()
+        R, ny = self.ranks, self.grids[0].shape[0] - 2
+        return all(torch.equal(self.grids[r][0].cpu(), self.grids[(r - 1) % R][ny].cpu()) and
+                   torch.equal(self.grids[r][ny + 1].cpu(), self.grids[(r + 1) % R][1].cpu())
+                   for r in range(R))
+
+
+def run_jacobi(spec: JacobiSpec, config: PathConfig, engine, compute: str = "model",
+               topology: str = "b200") -> BenchResult:
+    """Iterations of compute plus ring halo exchange against the single-path
+    baseline on the same problem (bench.py:355-390), measured on the GPU.
+
+    Every exchange is real: per phase, the four ring transfers go out as one
+    program (`Engine.send_many`, channel-disjoint staging through
+    plan_contention_free when the config has relays or the host path).
+    `compute="model"` adds `spec.compute_seconds` per iteration as the
+    reference does; `compute="kernel"` also runs a real 5-point Jacobi sweep
+    on every rank each iteration and adds its measured device time.  The
+    integrity row is 1.0 when every halo row equals its neighbour's boundary
+    row byte for byte after the last exchange of both arms."""
+    import torch
+    if len(engine.topology.accelerators) != spec.ranks:
+        raise ValueError(f"halo-exchange model needs a {spec.ranks}-accelerator topology, "
+                         f"{engine.topology.name!r} has {len(engine.topology.accelerators)}")
+    if compute not in ("model", "kernel"):
+        raise ValueError("compute is 'model' or 'kernel'")
+    bench_spec = BenchmarkSpec("jacobi", sizes=[spec.halo_bytes(nx) for nx in spec.nx_values],
+                               iterations=spec.iterations, config=config, topology=topology)
+    stream = torch.cuda.Stream(device=engine.device_map[0])
+    rows, all_clear = [], True
+    for nx in spec.nx_values:
+        halo = spec.halo_bytes(nx)
+        ring = _Ring(engine, spec, nx, stream)
+        comm, compute_s = {}, 0.0
+        for name, cfg in (("cfg", config), ("base", BASELINE_CONFIG)):
+            engine.clear_cache()
+            first = _iteration(engine, [lambda c=cfg: ring.exchange(c)], stream)
+            for _ in range(2):
+                _iteration(engine, [lambda c=cfg: ring.exchange(c)], stream)
+            steady = sum(_iteration(engine, [lambda c=cfg: ring.exchange(c)], stream)
+                         for _ in range(spec.timed)) / spec.timed
+            comm[name] = first + steady * (spec.iterations - 1)
+            all_clear &= ring.halos_match()
+        if compute == "kernel":
+            ring.compute()
+            compute_s = sum(_iteration(engine, [ring.compute], stream)
+                            for _ in range(spec.timed)) / spec.timed
+        per_iter = spec.compute_seconds(nx) + compute_s
+        runtime = per_iter * spec.iterations + comm["cfg"]
+        base_runtime = per_iter * spec.iterations + comm["base"]
+        rows.append(_row(bench_spec, config, halo, "runtime", runtime, base_runtime / runtime))
+        rows.append(_row(bench_spec, config, halo, "comm_time", comm["cfg"],
+                         comm["base"] / comm["cfg"]))
+        rows.append(_row(bench_spec, config, halo, "integrity", 1.0 if all_clear else 0.0))
+    return BenchResult(rows, integrity_all_clear=all_clear)

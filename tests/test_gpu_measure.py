@@ -30,3 +30,35 @@ def test_bw_bibw_latency_rows():
     plan = mp.make_chunk_plan(mp.plan_paths(topo, topo.device(0), topo.device(1), cfg), 1 << 20, 4)
     assert lat.value(1 << 20, "nodes") == mp.build_graph(plan).node_count
     eng.close()
+
+
+def test_jacobi_ring_exchange_is_exact_and_timed():
+    from paper_2604_22228_b200 import Engine, PathConfig
+    from paper_2604_22228_b200 import measure as M
+    eng = Engine.loopback(4)
+    nx = 1 << 20                                   # 2 MiB halo per neighbour
+    spec = M.JacobiSpec(nx_values=[nx], iterations=100, timed=4)
+    for cfg in (PathConfig(2, False, 4, graph_mode=True), PathConfig(1, True, 2),
+                PathConfig(3, True, 8, graph_mode=True)):
+        res = M.run_jacobi(spec, cfg, eng)
+        halo = spec.halo_bytes(nx)
+        assert res.integrity_all_clear and res.value(halo, "integrity") == 1.0
+        assert res.value(halo, "comm_time") > 0 and res.speedup(halo, "comm_time") > 0
+        assert res.value(halo, "runtime") == res.value(halo, "comm_time")  # no compute
+    modeled = M.JacobiSpec(nx_values=[nx], iterations=100, timed=4, compute_time_per_cell=1e-9)
+    res = M.run_jacobi(modeled, PathConfig(2, False, 4, graph_mode=True), eng, compute="kernel")
+    halo = modeled.halo_bytes(nx)
+    assert res.value(halo, "runtime") > res.value(halo, "comm_time") + 100 * \
+        modeled.compute_seconds(nx)
+    assert res.integrity_all_clear
+    assert len(res.to_csv().splitlines()) == 4
+    eng.close()
+
+
+def test_jacobi_needs_four_ranks():
+    from paper_2604_22228_b200 import Engine, PathConfig
+    from paper_2604_22228_b200 import measure as M
+    eng = Engine.loopback(2)
+    with pytest.raises(ValueError, match="4-accelerator"):
+        M.run_jacobi(M.JacobiSpec(nx_values=[1 << 20]), PathConfig(), eng)
+    eng.close()
