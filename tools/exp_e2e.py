@@ -10,15 +10,18 @@ import torch  # noqa: E402
 from paper_2604_22228_b200 import Engine, PathConfig, load_topology, mesh_text  # noqa: E402
 
 size, W, steps = 512 << 20, 64, 4
-topo = mesh_text("b200_loopback", 2, 3.17e12, 1, 2e-6, 4e9, 1e-5, "full")
+HOST_BWS = [float(x) * 1e9 for x in os.environ.get("HOST_BWS", "4").split(",")]
 src = torch.randint(0, 256, (size,), dtype=torch.uint8, device="cuda")
 dst = torch.empty_like(src)
 hsrc = torch.empty(size, dtype=torch.uint8, pin_memory=True)
 hsrc.copy_(src.cpu())
 cur = torch.cuda.current_stream()
 cs = torch.cuda.Stream()
-for host in ("ce", "sm"):
-    for paths in ("direct+host", "direct"):
+variants = [(h, "direct+host", bw) for h in ("ce", "sm") for bw in HOST_BWS] + \
+    [("ce", "direct", 4e9)]
+for host, paths, hbw in variants:
+    if True:
+        topo = mesh_text("b200_loopback", 2, 3.17e12, 1, 2e-6, hbw, 1e-5, "full")
         eng = Engine(load_topology(topo), [0, 0])
         eng.configure(host=host)
         cfg = PathConfig(1, paths == "direct+host", 8, True)
@@ -55,6 +58,6 @@ for host in ("ce", "sm"):
         e1.record(cur)
         torch.cuda.synchronize()
         t2 = e0.elapsed_time(e1) / 1e3
-        print(f"host={host} {paths}: e2e {steps * W * size / t / 1e9:.1f} GB/s, "
+        print(f"host={host} {paths} host_bw={hbw / 1e9:g}: e2e {steps * W * size / t / 1e9:.1f} GB/s, "
               f"sends alone {steps * W * size / t2 / 1e9:.1f} GB/s", flush=True)
         eng.close()
