@@ -104,7 +104,35 @@ static PyObject* fast_bind(PyObject* self, PyObject* const* args, Py_ssize_t nar
   return (PyObject*)b;
 }
 
+/* mp_send_many over a caller-owned mp_xfer array (Engine.prepare_many keeps
+ * the array and config alive): send_many(ctx, xfers, n, cfg, joint, stream). */
+static PyObject* fast_send_many(PyObject* self, PyObject* const* args, Py_ssize_t nargs) {
+  (void)self;
+  if (nargs != 6) {
+    PyErr_SetString(PyExc_TypeError, "send_many(ctx, xfers, n, cfg, joint, stream)");
+    return NULL;
+  }
+  mp_ctx* ctx = (mp_ctx*)PyLong_AsVoidPtr(args[0]);
+  const mp_xfer* xs = (const mp_xfer*)PyLong_AsVoidPtr(args[1]);
+  long n = PyLong_AsLong(args[2]);
+  const mp_config* cfg = (const mp_config*)PyLong_AsVoidPtr(args[3]);
+  long joint = PyLong_AsLong(args[4]);
+  void* stream = PyLong_AsVoidPtr(args[5]);
+  if (PyErr_Occurred()) return NULL;
+  if (n < INT32_MIN || n > INT32_MAX) {
+    PyErr_SetString(PyExc_OverflowError, "transfer count out of range");
+    return NULL;
+  }
+  int rc;
+  Py_BEGIN_ALLOW_THREADS
+  rc = mp_send_many(ctx, xs, (int32_t)n, cfg, joint ? 1 : 0, stream);
+  Py_END_ALLOW_THREADS
+  return PyLong_FromLong(rc);
+}
+
 static PyMethodDef methods[] = {
+    {"send_many", (PyCFunction)(void (*)(void))fast_send_many, METH_FASTCALL,
+     "mp_send_many over an mp_xfer array address; returns the MP_* status"},
     {"send", (PyCFunction)(void (*)(void))fast_send, METH_FASTCALL,
      "mp_send with integer arguments; returns the MP_* status"},
     {"bind", (PyCFunction)(void (*)(void))fast_bind, METH_FASTCALL,

@@ -258,14 +258,9 @@ class Engine:
         launch.bound = bound  # the raw C callable (returns the MP_* status)
         return launch
 
-    def send_many(self, transfers, config: PathConfig | None = None, joint: bool = False,
-                  stream=None) -> None:
-        """Concurrent transfers as one program (windows, bidirectional flows,
-        ring halo exchanges): `transfers` = [(src, dst, nbytes, src_dev, dst_dev)]
-        with tensors; nbytes None = all of src.  joint=True picks channel-
-        disjoint staging devices (plan_contention_free, paths.py:210-242)."""
+    def _xfers(self, transfers, stream):
+        """(mp_xfer array, stream handle) for send_many / prepare_many."""
         torch = _torch()
-        config = config or PathConfig.from_env()
         arr = (_lib.mp_xfer * len(transfers))()
         first = None
         for i, (src, dst, nbytes, sd, dd) in enumerate(transfers):
@@ -279,9 +274,43 @@ class Engine:
         if stream is None:
             stream = torch.cuda.current_stream(first.device)
         handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        return arr, handle
+
+    def send_many(self, transfers, config: PathConfig | None = None, joint: bool = False,
+                  stream=None) -> None:
+        """Concurrent transfers as one program (windows, bidirectional flows,
+        ring halo exchanges): `transfers` = [(src, dst, nbytes, src_dev, dst_dev)]
+        with tensors; nbytes None = all of src.  joint=True picks channel-
+        disjoint staging devices (plan_contention_free, paths.py:210-242)."""
+        config = config or PathConfig.from_env()
+        arr, handle = self._xfers(transfers, stream)
         cfg = config.abi()
         check(lib.mp_send_many(self._ctx, arr, len(transfers), C.byref(cfg), int(joint),
                                handle or None))
+
+    def prepare_many(self, transfers, config: PathConfig | None = None, joint: bool = False,
+                     stream=None):
+        """`send_many` bound once (same arguments): returns a zero-argument
+        callable that posts the program with one C call — a window of W
+        messages costs one host call and, on a cached hit, one graph launch.
+        The binding keeps the tensors, config and stream alive; it must not
+        outlive the engine."""
+        config = config or PathConfig.from_env()
+        arr, handle = self._xfers(transfers, stream)
+        keep = (list(transfers), config, stream, arr)
+        args = (self._ctx_addr, C.addressof(arr), len(transfers), config.abi_addr(), int(joint),
+                handle or 0)
+        ctx, send_many = self._ctx_addr, _mpfast.send_many
+        engine = self
+
+        def launch() -> None:
+            if engine._ctx_addr != ctx:  # closed engine: never touch a freed context
+                raise EngineError("prepared send used after Engine.close()")
+            rc = send_many(*args)
+            if rc:
+                check(rc)
+        launch.keep = keep
+        return launch
 
     def recv(self, dst, stream=None) -> None:
         """Single-process mode: `send` already wrote `dst` on the sender's

@@ -134,20 +134,43 @@ def _measure(engine, spec, posts, stream):
     return first, sum(times) / len(times)
 
 
-def run_bw(spec: BenchmarkSpec, engine, src_dev: int = 0, dst_dev: int = 1) -> BenchResult:
-    """Unidirectional bandwidth with a posting window (bench.py:185-210), measured."""
+MAX_PROGRAM = 64  # transfers per mp_send_many program (include/mpb200.h)
+
+
+def run_bw(spec: BenchmarkSpec, engine, src_dev: int = 0, dst_dev: int = 1,
+           program: bool = False) -> BenchResult:
+    """Unidirectional bandwidth with a posting window (bench.py:185-210), measured.
+
+    program=False: the W messages of a window are W `send` calls on one
+    src/dst pair (osu_bw re-sends one buffer).  program=True: the window is
+    posted as ONE `send_many` program over W distinct src/dst pairs (like a
+    grouped ncclSend, one launch per window); the baseline is still per-call
+    BASELINE_CONFIG sends over the same W pairs."""
     import torch
+    if program and not 1 <= spec.window <= MAX_PROGRAM:
+        raise ValueError(f"a program window holds 1..{MAX_PROGRAM} messages")
     rows = []
     stream = torch.cuda.Stream(device=engine.device_map[src_dev])
     for size in spec.sizes:
-        (src, dst), = _buffers(engine, size)
+        pairs = _buffers(engine, size, spec.window if program else 1)
+        src, dst = pairs[0]
 
         def sweep(cfg):
             engine.clear_cache()
-            post = lambda: engine.send(src, dst, size, cfg, stream=stream,  # noqa: E731
-                                       src_dev=src_dev, dst_dev=dst_dev)
-            return _measure(engine, spec, [post] * spec.window, stream)
+            if program and cfg is spec.config:
+                post = engine.prepare_many([(s, d, size, src_dev, dst_dev) for s, d in pairs],
+                                           cfg, stream=stream)
+                return _measure(engine, spec, [post], stream)
+            posts = [lambda s=s, d=d: engine.send(s, d, size, cfg, stream=stream, src_dev=src_dev,
+                                                  dst_dev=dst_dev)
+                     for s, d in (pairs if program else pairs * spec.window)]
+            return _measure(engine, spec, posts, stream)
+        for s, d in pairs:
+            d.copy_(torch.bitwise_not(s))
         first, mean = sweep(spec.config)
+        torch.cuda.synchronize()
+        if not all(torch.equal(s, d) for s, d in pairs):
+            raise RuntimeError(f"{spec.kind}: delivered bytes differ at size {size}")
         base_first, base_mean = sweep(BASELINE_CONFIG)
         bw, base_bw = spec.window * size / mean, spec.window * size / base_mean
         rows.append(_row(spec, spec.config, size, "bandwidth", bw, bw / base_bw))

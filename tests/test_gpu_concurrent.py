@@ -50,6 +50,28 @@ def test_window_of_messages(graph):
     eng.close()
 
 
+@pytest.mark.parametrize("host", [False, True])
+def test_prepared_window(host):
+    """prepare_many: a bound program resent several times is byte-exact each
+    time, and refuses to run after the engine is closed."""
+    from paper_2604_22228_b200 import EngineError, PathConfig
+    eng = _engine(2)
+    sizes = [1, 4096 + 3, 65536, MiB + 17] * 16  # a 64-message window
+    srcs, dsts, datas = _bufs(sizes, 11)
+    post = eng.prepare_many([(s, d, None, 0, 1) for s, d in zip(srcs, dsts)],
+                            PathConfig(host_path_enabled=host, max_chunks=2, graph_mode=True))
+    for rep in range(3):
+        post()
+        eng.sync()
+        for d, want in zip(dsts, datas):
+            assert np.array_equal(d.cpu().numpy(), want)
+        for d in dsts:
+            d.fill_(0)
+    eng.close()
+    with pytest.raises(EngineError):
+        post()
+
+
 @pytest.mark.parametrize("relay", ["sm", "ce"])
 def test_bidirectional_flows(relay):
     from paper_2604_22228_b200 import PathConfig

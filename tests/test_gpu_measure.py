@@ -32,6 +32,23 @@ def test_bw_bibw_latency_rows():
     eng.close()
 
 
+@pytest.mark.parametrize("window", [1, 16, 64])
+def test_program_window_is_exact(window):
+    """A window posted as one send_many program over W distinct pairs: every
+    pair byte-exact (run_bw checks), odd and tiny sizes included."""
+    from paper_2604_22228_b200 import Engine, PathConfig
+    from paper_2604_22228_b200 import measure as M
+    eng = Engine.loopback(2)
+    sizes = [1, 4096 + 3, 65536, (1 << 20) + 12345]
+    res = M.run_bw(M.BenchmarkSpec("omb_bw_program", sizes, window=window, iterations=2,
+                                   warmup=1, config=PathConfig(1, False, 1, True)), eng,
+                   program=True)
+    assert res.value(65536, "bandwidth") > 0.0
+    with pytest.raises(ValueError):
+        M.run_bw(M.BenchmarkSpec("omb_bw_program", [4096], window=65), eng, program=True)
+    eng.close()
+
+
 def test_jacobi_ring_exchange_is_exact_and_timed():
     from paper_2604_22228_b200 import Engine, PathConfig
     from paper_2604_22228_b200 import measure as M
