@@ -171,7 +171,11 @@ def run_bw(spec: BenchmarkSpec, engine, src_dev: int = 0, dst_dev: int = 1,
         torch.cuda.synchronize()
         if not all(torch.equal(s, d) for s, d in pairs):
             raise RuntimeError(f"{spec.kind}: delivered bytes differ at size {size}")
-        base_first, base_mean = sweep(BASELINE_CONFIG)
+        # W distinct pairs are W cache keys: the baseline's cache holds them
+        # all (an LRU smaller than the window would rebuild every send)
+        base_cfg = replace(BASELINE_CONFIG, cache_capacity=max(BASELINE_CONFIG.cache_capacity,
+                                                                len(pairs)))
+        base_first, base_mean = sweep(base_cfg)
         bw, base_bw = spec.window * size / mean, spec.window * size / base_mean
         rows.append(_row(spec, spec.config, size, "bandwidth", bw, bw / base_bw))
         rows.append(_row(spec, spec.config, size, "first_iteration_makespan", first))
