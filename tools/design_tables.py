@@ -35,3 +35,15 @@ if w:
             v = per[str(s)]
             cells.append(f"{fmt(v['single'])} / {fmt(v['multi_k8'])} / {fmt(v['baseline'])}")
         print(f"| {win} | " + " | ".join(cells) + " |")
+    if any("single_program" in v for per in w["gbs"].values() for v in per.values()):
+        print()
+        print("| W | " + " | ".join(label(s) for s in sizes) + " |")
+        print("|---|" + "---|" * len(sizes))
+        for win, per in w["gbs"].items():
+            cells = []
+            for s in sizes:
+                v = per[str(s)]
+                cells.append(f"**{fmt(v['single_program'])}** / {fmt(v['single'])} / "
+                             f"{fmt(v['baseline_distinct_buffers'])}"
+                             if "single_program" in v else "—")
+            print(f"| {win} | " + " | ".join(cells) + " |")
