@@ -183,6 +183,27 @@ struct Program {
   std::shared_ptr<mpk::SmallTable<mpk::kSmallMaxTiles>> small;  // PROG_SMALL: the table as kernel params
 };
 
+// Hash of a cache key (raw bytes: pointers, sizes, devices, config; up to
+// 64 transfers for a program): 8 bytes per step, a few ns per transfer —
+// std::hash<std::string> costs ~1 us on a 64-transfer key.
+struct KeyHash {
+  size_t operator()(const std::string& k) const noexcept {
+    const char* p = k.data();
+    size_t n = k.size();
+    uint64_t h = 0x9E3779B97F4A7C15ull ^ n;
+    for (; n >= 8; p += 8, n -= 8) {
+      uint64_t w;
+      memcpy(&w, p, 8);
+      h = (h ^ w) * 0xff51afd7ed558ccdull;
+      h ^= h >> 32;
+    }
+    uint64_t w = 0;
+    memcpy(&w, p, n);
+    h = (h ^ w) * 0xc4ceb9fe1a85ec53ull;
+    return (size_t)(h ^ (h >> 29));
+  }
+};
+
 struct Entry {
   std::string key;
   std::vector<mp_path> paths;
@@ -231,7 +252,7 @@ struct mp_ctx {
   uint8_t* host_stage = nullptr;
   size_t host_cap = 0;
   std::list<Entry*> lru;  // least recent first
-  std::unordered_map<std::string, std::list<Entry*>::iterator> index;
+  std::unordered_map<std::string, std::list<Entry*>::iterator, KeyHash> index;
   mp_send_stats stats{};
   std::vector<mp_path> last_paths;
   std::vector<mp_chunk> last_chunks;

@@ -275,7 +275,8 @@ class Lowering {
     if (o_.sched != MP_SCHED_AUTO || o_.tile_bytes != 0) return;
     std::vector<uint64_t> sm_bytes(nph, 0);
     std::vector<int> segs(nph, 0);
-    std::vector<char> dyn(nph, 0);
+    std::vector<char> dyn(nph, 0), relayed(nph, 0);
+    std::vector<std::vector<std::pair<uint64_t, uint64_t>>> direct_segs(nph);  // (dst, len)
     for (int t = 0; t < T; ++t) {
       const int sp = phys_of(xs_[t].sd), dp = phys_of(xs_[t].dd);
       for (const mp_chunk& c : chunks_[t]) {
@@ -284,9 +285,11 @@ class Lowering {
           const int ex = o_.pull ? dp : sp;
           sm_bytes[ex] += c.length;
           segs[ex] += 1;
+          direct_segs[ex].emplace_back((uint64_t)(uintptr_t)xs_[t].dst + c.offset, c.length);
         } else if (P.kind == MP_PATH_GPU && eng_[t].relay_sm) {
           sm_bytes[sp] += c.length;
           segs[sp] += 1;
+          relayed[sp] = 1;
           dyn[phys_of(P.stage)] = 1;
         } else if (P.kind == MP_PATH_HOST && eng_[t].host_sm) {
           dyn[sp] = dyn[dp] = 1;
@@ -295,7 +298,25 @@ class Lowering {
     }
     for (size_t ph = 0; ph < nph; ++ph) {
       const uint64_t grid = (uint64_t)ctx_->phys[ph].sms;
-      if (dyn[ph] || segs[ph] == 0 || (uint64_t)segs[ph] * 4 > grid) continue;
+      if (dyn[ph] || segs[ph] == 0) continue;
+      if ((uint64_t)segs[ph] * 4 > grid) {
+        // many small direct segments (a posting window sent as one program,
+        // mp_send_many): the small-message kernel still takes them in ONE
+        // launch slot if a tile size keeps the table within one tile per
+        // SM — the smallest 16-byte multiple that does, counted exactly
+        if (relayed[ph] || (uint64_t)segs[ph] > grid || sm_bytes[ph] > (uint64_t)o_.small_max_bytes)
+          continue;
+        uint64_t tb = std::max<uint64_t>((sm_bytes[ph] + grid - 1) / grid, kStaticMinTile);
+        for (;; tb += tb / 4) {
+          tb = (tb + 15) & ~(uint64_t)15;
+          uint64_t n = 0;
+          for (const auto& sg : direct_segs[ph]) n += ntiles_of(sg.first, sg.second, tb);
+          if (n <= grid) break;
+        }
+        static_tile_[ph] = tb;
+        static_kind_[ph] = PROG_SMALL;
+        continue;
+      }
       const bool small = sm_bytes[ph] <= (uint64_t)o_.small_max_bytes;
       const bool tma = sm_bytes[ph] <= grid * kStaticMaxPerCta && tma_ok(o_, peer_phys_[ph] != 0);
       if (!small && !tma) continue;

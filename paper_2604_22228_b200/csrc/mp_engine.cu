@@ -212,14 +212,21 @@ void capture(mp_ctx* ctx, Entry* e) {
   ctx->stats.instantiation_us = t3 - t2;
 }
 
-std::string make_key(const void* src, void* dst, uint64_t size, int sd, int dd, const mp_config& c) {
+void append_key(std::string& key, const void* src, void* dst, uint64_t size, int sd, int dd,
+                const mp_config& c) {
   struct {
     uint64_t s, d, n;
     int32_t sd, dd, g, h, m, gm, pol, pad;  // explicit pad: every key byte is defined
   } k{(uint64_t)(uintptr_t)src, (uint64_t)(uintptr_t)dst, size, sd, dd,
       c.num_gpu_paths, c.host_path_enabled, c.max_chunks, c.graph_mode ? 1 : 0, c.share_policy, 0};
   static_assert(sizeof k == 3 * 8 + 8 * 4, "key has no implicit padding");
-  return std::string((const char*)&k, sizeof k);
+  key.append((const char*)&k, sizeof k);
+}
+
+std::string make_key(const void* src, void* dst, uint64_t size, int sd, int dd, const mp_config& c) {
+  std::string key;
+  append_key(key, src, dst, size, sd, dd, c);
+  return key;
 }
 
 // LRU lookup; a miss plans, lowers and (graph mode) captures + instantiates
@@ -230,7 +237,8 @@ Entry* lookup_entry(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int 
                     const std::function<Entry*(const std::string&)>& builder = nullptr,
                     const std::string* key_override = nullptr) {
   double t_start = now_us();
-  std::string key = key_override ? *key_override : make_key(src, dst, size, src_dev, dst_dev, cfg);
+  std::string own;
+  const std::string& key = key_override ? *key_override : (own = make_key(src, dst, size, src_dev, dst_dev, cfg));
   mp_send_stats& st = ctx->stats;
   auto it = ctx->index.find(key);
   if (it != ctx->index.end()) {
@@ -673,8 +681,10 @@ int mp_send_many(mp_ctx* ctx, const mp_xfer* xfers, int32_t n, const mp_config* 
   if (!ctx || !cfg || !xfers || n < 1 || n > 64) return fail(MP_ERR_VALUE, "need 1..64 transfers");
   if (!ctx->has_topo) return fail(MP_ERR_STATE, "context has no topology (mp_ctx_set_topology)");
   if (ctx->group) return fail(MP_ERR_STATE, "group context: use mp_group_send");
-  std::vector<Xfer> xs;
-  std::string key = joint ? "J" : "I";
+  // the key is built in a reused buffer (a cached-graph hit allocates
+  // nothing: a 64-message window is one host call of a few us)
+  thread_local std::string key;
+  key.assign(1, joint ? 'J' : 'I');
   for (int i = 0; i < n; ++i) {
     const mp_xfer& x = xfers[i];
     if (x.src_dev < 0 || x.src_dev >= (int)ctx->logi.size() || x.dst_dev < 0 ||
@@ -682,15 +692,17 @@ int mp_send_many(mp_ctx* ctx, const mp_xfer* xfers, int32_t n, const mp_config* 
       return fail(MP_ERR_PLAN, "transfers run between accelerators");
     if (x.size == 0) return fail(MP_ERR_CHUNK, "message size must be >= 1 byte, got 0");
     if (!x.src || !x.dst) return fail(MP_ERR_VALUE, "null buffer");
-    xs.push_back(Xfer{x.src, x.dst, x.size, x.src_dev, x.dst_dev, {}});
-    key += make_key(x.src, x.dst, x.size, x.src_dev, x.dst_dev, *cfg);
+    append_key(key, x.src, x.dst, x.size, x.src_dev, x.dst_dev, *cfg);
   }
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
   cudaStream_t user = (cudaStream_t)stream;
   Entry* e = lookup_entry(
-      ctx, xs[0].src, xs[0].dst, xs[0].size, xs[0].sd, xs[0].dd, *cfg, user,
+      ctx, xfers[0].src, xfers[0].dst, xfers[0].size, xfers[0].src_dev, xfers[0].dst_dev, *cfg, user,
       [&](const std::string& k) {
+        std::vector<Xfer> xs;
+        for (int i = 0; i < n; ++i)
+          xs.push_back(Xfer{xfers[i].src, xfers[i].dst, xfers[i].size, xfers[i].src_dev, xfers[i].dst_dev, {}});
         if (joint) {  // channel-disjoint staging across the transfers (paths.py:210-242)
           std::vector<std::pair<int, int>> tr;
           for (auto& x : xs) tr.emplace_back(x.sd, x.dd);
