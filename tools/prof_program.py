@@ -27,5 +27,14 @@ for _ in range(100):
 e1.record(s)
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) / 100 * 1e3
+# host cost of posting a window: batches of 50 posts, synced between batches
+import time  # noqa: E402
+host = 0.0
+for _ in range(20):
+    t0 = time.perf_counter()
+    for _ in range(50):
+        post()
+    host += time.perf_counter() - t0
+    s.synchronize()
 print(f"W={W} x {size} B: {us:.2f} us per window back to back = {W * size / us / 1e3:.1f} GB/s; "
-      f"kernel {eng.stats().kernel}")
+      f"host {host / 1000 * 1e6:.2f} us per post; kernel {eng.stats().kernel}")
