@@ -256,6 +256,17 @@ struct mp_ctx {
   mp_send_stats stats{};
   std::vector<mp_path> last_paths;
   std::vector<mp_chunk> last_chunks;
+  // resend fast path of mp_send_many: the last program's raw arguments and
+  // its entry, valid while no entry has been destroyed since (cache_epoch)
+  uint64_t cache_epoch = 0;
+  struct {
+    std::vector<mp_xfer> xfers;
+    mp_config cfg{};
+    int32_t joint = -1;
+    Entry* entry = nullptr;
+    std::list<Entry*>::iterator lru_pos;
+    uint64_t epoch = 0;
+  } last_many;
   cudaEvent_t last_done = nullptr;  // serialises sends issued on different streams
   void* last_stream = nullptr;
   bool have_last = false;
@@ -295,6 +306,7 @@ cudaStream_t lane_stream(Phys& p, int lane) {
 
 void destroy_entry(mp_ctx* ctx, Entry* e) {
   if (!e) return;
+  ctx->cache_epoch++;  // invalidates every remembered Entry* (mp_send_many fast path)
   for (auto& pr : e->progs) {
     cudaSetDevice(ctx->phys[pr.phys].ordinal);
     if (pr.d_tiles) cudaFree(pr.d_tiles);
@@ -311,6 +323,7 @@ void clear_cache(mp_ctx* ctx) {
   for (Entry* e : ctx->lru) destroy_entry(ctx, e);
   ctx->lru.clear();
   ctx->index.clear();
+  ctx->cache_epoch++;
 }
 
 // Grow staging arenas; cached programs point into them, so growth drops the cache.

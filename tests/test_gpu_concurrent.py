@@ -72,6 +72,40 @@ def test_prepared_window(host):
         post()
 
 
+def test_program_resend_fast_path_follows_the_cache():
+    """mp_send_many remembers the last program's arguments and entry; the
+    memo must follow evictions, cache clears and other programs: every
+    resend is byte-exact and hit/miss is what the LRU says."""
+    from paper_2604_22228_b200 import PathConfig
+    eng = _engine(2)
+    srcs, dsts, datas = _bufs([4096 + 1, 70000, 3 * MiB + 5, 17], 21)
+    cfg = PathConfig(max_chunks=2, graph_mode=True, cache_capacity=1)
+    prog_a = [(srcs[0], dsts[0], None, 0, 1), (srcs[1], dsts[1], None, 0, 1)]
+    prog_b = [(srcs[2], dsts[2], None, 0, 1), (srcs[3], dsts[3], None, 0, 1)]
+
+    def post(prog, want_hit):
+        for _, d, _, _, _ in prog:
+            d.zero_()
+        eng.send_many(prog, cfg)
+        eng.sync()
+        assert eng.stats().hit == want_hit
+        for s, d, _, _, _ in prog:
+            assert torch.equal(s, d)
+
+    post(prog_a, 0)
+    post(prog_a, 1)                    # fast path
+    post(prog_b, 0)                    # capacity 1: evicts A
+    post(prog_a, 0)                    # memo of A is stale: rebuilt
+    post(prog_a, 1)
+    eng.send(srcs[3], dsts[3], None, cfg, src_dev=0, dst_dev=1)   # evicts A
+    eng.sync()
+    post(prog_a, 0)
+    eng.clear_cache()
+    post(prog_a, 0)
+    post(prog_a, 1)
+    eng.close()
+
+
 @pytest.mark.parametrize("relay", ["sm", "ce"])
 def test_bidirectional_flows(relay):
     from paper_2604_22228_b200 import PathConfig
