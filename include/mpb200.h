@@ -318,7 +318,9 @@ typedef struct {
  * tiles of every transfer share one persistent kernel per device,
  * interleaved round by round, and the whole batch is one cached graph.
  * joint = 1 chooses staging devices with plan_contention_free
- * (paths.py:210-242); 0 plans each transfer with plan_paths. */
+ * (paths.py:210-242); 0 plans each transfer with plan_paths.  1..64
+ * transfers.  Resending the previous call's exact arguments while its
+ * entry is cached skips the key rebuild (the osu_bw / halo-exchange loop). */
 int mp_send_many(mp_ctx* ctx, const mp_xfer* xfers, int32_t n, const mp_config* cfg,
                  int32_t joint, void* stream);
 
