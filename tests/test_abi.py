@@ -89,6 +89,25 @@ def test_cpython_fast_send_keeps_the_abi_contract():
         _mpfast.send(0, 0, 0)
 
 
+def test_cpython_fast_send_many_keeps_the_abi_contract():
+    """`_mpfast.send_many` (prepare_many's per-window call) is mp_send_many:
+    null context / out-of-range counts return MP_ERR_VALUE with the reason."""
+    import pytest
+
+    from paper_2604_22228_b200 import PathConfig, _mpfast
+    cfg = PathConfig()
+    xs = (_lib.mp_xfer * 2)()
+    import ctypes
+    for n in (2, 0, 65):
+        rc = _mpfast.send_many(0, ctypes.addressof(xs), n, cfg.abi_addr(), 0, 0)
+        assert rc == _lib.MP_ERR_VALUE
+        assert "1..64 transfers" in _lib.last_error()
+    with pytest.raises(TypeError):
+        _mpfast.send_many(0, 0)
+    with pytest.raises(OverflowError):
+        _mpfast.send_many(0, ctypes.addressof(xs), 1 << 40, cfg.abi_addr(), 0, 0)
+
+
 def test_path_config_abi_cache_pickles():
     import pickle
 
