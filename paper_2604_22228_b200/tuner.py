@@ -194,13 +194,21 @@ def tune_engines(engine, sizes: list[int], reps: int = 10, mode: str = GRAPH_MOD
     return rules, trials
 
 
+def pick_host_rate(runs, tolerance: float = 0.005):
+    """Of calibration runs (seconds, host_bw, ...), the one with the smallest
+    host rate whose time is within `tolerance` of the fastest (ties: faster)."""
+    fastest = min(r[0] for r in runs)
+    return min((r for r in runs if r[0] <= fastest * (1 + tolerance)), key=lambda r: (r[1], r[0]))
+
+
 def calibrate_host_bandwidth(engine, link_bw: float, size: int, max_chunks: int,
                              candidates: list[float] | None = None, reps: int = 10,
                              name: str = "calibrated",
-                             host_engines: tuple[str, ...] = ("ce", "sm")
-                             ) -> tuple[float, Topology, list]:
+                             host_engines: tuple[str, ...] = ("ce", "sm"),
+                             tolerance: float = 0.005) -> tuple[float, Topology, list]:
     """Pick the host-link bandwidth for the `.topo` (and the host-path
-    mechanism) that maximise the measured direct+host throughput at `size`.
+    mechanism) that maximise the measured direct+host throughput at `size`
+    (the smallest host rate within `tolerance` of the best).
     Leaves `engine` on the winning topology and host mechanism; returns
     (host_bw, topology, trials) with trials = [(engine, host_bw, GB/s)]."""
     import torch
@@ -213,7 +221,7 @@ def calibrate_host_bandwidth(engine, link_bw: float, size: int, max_chunks: int,
     stream = torch.cuda.Stream(device=dev)
     cfg = PathConfig(1, True, max_chunks, True)
     trials = []
-    best = None
+    runs = []
     for host in host_engines:
         engine.configure(host=host)
         for bw in candidates:
@@ -221,8 +229,12 @@ def calibrate_host_bandwidth(engine, link_bw: float, size: int, max_chunks: int,
             engine.set_topology(topo)
             t = measure_makespan(engine, cfg, size, src, dst, stream, reps)
             trials.append((host, bw, size / t / 1e9))
-            if best is None or t < best[0]:
-                best = (t, bw, topo, host)
+            runs.append((t, bw, topo, host))
+    # the curve is flat over a wide range of host rates (an HBM-bound copy):
+    # take the smallest host rate within `tolerance` of the fastest, so run
+    # noise does not pick a large host share that other configurations (more
+    # paths, other sizes planned from the same .topo) then pay for
+    best = pick_host_rate(runs, tolerance)
     engine.configure(host=best[3])
     engine.set_topology(best[2])
     return best[1], best[2], trials

@@ -34,3 +34,15 @@ def test_result_rows_and_speedup_lookup():
     with pytest.raises(KeyError, match="no speedup"):
         res.speedup(MiB, "integrity")
     assert res.to_csv().splitlines()[1] == "jacobi,b200,1048576,1,2,off,on,4,comm_time,0.001,1.5"
+
+
+def test_host_rate_pick_prefers_the_smallest_within_tolerance():
+    """The calibration curve is flat over a wide range of host rates; the
+    pick is the smallest host rate within tolerance of the fastest run."""
+    from paper_2604_22228_b200.tuner import pick_host_rate
+    runs = [(1.000, 1e9, "t1", "ce"), (0.998, 4e9, "t4", "ce"), (0.996, 16e9, "t16", "ce"),
+            (1.200, 55e9, "t55", "ce"), (0.999, 2e9, "t2", "sm")]
+    assert pick_host_rate(runs, 0.005)[1] == 1e9
+    assert pick_host_rate(runs, 0.0025)[1:3] == (4e9, "t4")
+    assert pick_host_rate(runs, 0.0)[1] == 16e9
+    assert pick_host_rate([(2.0, 8e9, "a", "sm")])[1] == 8e9
