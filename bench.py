@@ -545,10 +545,13 @@ def run_sweep(torch, eng, topo_text, dev, stream):
     # measured per-size choices: direct mechanism (SM kernel vs CE), then the
     # reference tuner's grid (paths x host x chunks) on top of it
     auto = Engine(load_topology(topo_text), [dev, dev])
-    rules, _ = tune_engines(auto, SWEEP_SIZES, reps=10)
+    # 50 back-to-back sends per trial: the steady state the sweep measures
+    # (10-send bursts favoured the copy engine at ~1 MiB, which then lost
+    # to the SM kernel over the sweep's 200-send runs)
+    rules, _ = tune_engines(auto, SWEEP_SIZES, reps=50)
     auto.set_size_policy(rules)
     grid = [GridPoint(1, h, c) for h in (False, True) for c in (1, 2, 4, 8, 16, 32)]
-    table = tune(auto, SWEEP_SIZES, grid, modes=("graph",), reps=10)
+    table = tune(auto, SWEEP_SIZES, grid, modes=("graph",), reps=50)
     rows = []
     big = torch.empty(SWEEP_SIZES[-1], dtype=torch.uint8, device=f"cuda:{dev}")
     out = torch.empty_like(big)
