@@ -112,7 +112,7 @@ def measure_makespan(engine, config: PathConfig, size: int, src, dst, stream,
 
 
 def tune(engine, sizes: list[int], grid: list[GridPoint] | None = None,
-         modes: tuple[str, ...] = MODES, reps: int = 10, device=None) -> TuningTable:
+         modes: tuple[str, ...] = MODES, reps: int = 50, device=None) -> TuningTable:
     """Time every grid point per (size, mode) on the GPU; record the argmin."""
     import torch
     if not sizes:
@@ -142,7 +142,7 @@ def tune(engine, sizes: list[int], grid: list[GridPoint] | None = None,
     return TuningTable(engine.topology.name, entries)
 
 
-def tune_engines(engine, sizes: list[int], reps: int = 10, mode: str = GRAPH_MODE,
+def tune_engines(engine, sizes: list[int], reps: int = 50, mode: str = GRAPH_MODE,
                  host_chunks: int = 2) -> tuple[list[tuple[int, str, str]], list[dict]]:
     """Measure, at every size, the direct path by the SM transfer kernel vs a
     copy-engine copy (single path), then — with the winning direct mechanism —
