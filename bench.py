@@ -534,10 +534,31 @@ def run_ours(args, rank, world):
 SWEEP_SIZES = [1 << k for k in range(10, 30)]
 
 
+def time_prepared(torch, eng, cfg, src, dst, size, steps, warmup, stream, trials=3):
+    """time_sends for a send bound once (Engine.prepare): osu_bw re-sends one
+    buffer, so the per-message host cost is one C call."""
+    go = eng.prepare(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
+    for _ in range(max(5, warmup)):
+        go()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = None
+    for _ in range(trials):
+        e0.record(stream)
+        for _ in range(steps):
+            go()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3 / steps
+        best = t if best is None else min(best, t)
+    return best
+
+
 def run_sweep(torch, eng, topo_text, dev, stream):
-    """osu_bw-style: per size, single path (CE copy = cudaMemcpy, SM kernel),
-    direct+host multi-path with the graph cache on / off, and the measured
-    tuner's best configuration."""
+    """osu_bw-style: per size, single path (CE copy = cudaMemcpy, SM kernel;
+    the SM send also bound once with Engine.prepare), direct+host multi-path
+    with the graph cache on / off, and the measured tuner's best
+    configuration."""
     from paper_2604_22228_b200 import Engine, PathConfig, load_topology
     from paper_2604_22228_b200.tuner import GridPoint, tune, tune_engines
     ce = Engine(load_topology(topo_text), [dev, dev])
@@ -570,6 +591,9 @@ def run_sweep(torch, eng, topo_text, dev, stream):
             kernels[name] = e.stats().kernel.split(" ")[0] or "copy engine"
         row["kernels"] = kernels
         best = table.lookup(size, "graph").best
+        row["sm_single_prepared"] = size / time_prepared(
+            torch, eng, PathConfig(max_chunks=1, graph_mode=True), src, dst, size, steps, warm,
+            stream) / 1e9
         row["tuned"] = size / time_sends(torch, auto, table.config_for(size), src, dst, size,
                                          steps, warm, stream) / 1e9
         row["tuned_point"] = [best.gpu_paths, best.host, best.max_chunks,

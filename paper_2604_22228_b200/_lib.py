@@ -112,7 +112,8 @@ class mp_engine_opts(C.Structure):
                 ("tile_bytes", C.c_int64), ("host_slots", C.c_int32), ("pull", C.c_int32),
                 ("sm_min_bytes", C.c_int64), ("unroll", C.c_int32), ("tma_stages", C.c_int32),
                 ("tma_block", C.c_int32), ("host_engine", C.c_int32), ("tma_peer", C.c_int32),
-                ("sched", C.c_int32), ("small_max_bytes", C.c_int64)]
+                ("sched", C.c_int32), ("small_max_bytes", C.c_int64),
+                ("pdl", C.c_int32), ("reserved", C.c_int32)]
 
 
 P = C.POINTER

@@ -44,6 +44,9 @@ size_t kernel_smem(const mp_engine_opts& o) {
 // Tables that touch another GPU's memory never run TMA unless tma_peer allows
 // it (TMA bulk copies on peer addresses are unverified on this 1-GPU pool).
 enum ProgKind { PROG_DYNAMIC = 0, PROG_STATIC_TMA = 1, PROG_SMALL = 2 };
+// Small-message tables from this size launch with programmatic dependent
+// launch when opts.pdl is set (see pdl_replay in mp_engine.cu).
+constexpr uint64_t kPdlMinBytes = 1 << 20;
 constexpr int kPeerCtasPerSm = 4;
 constexpr uint64_t kVecTileBytes = 64 << 10;
 bool tma_ok(const mp_engine_opts& o, bool peer) {
@@ -83,16 +86,28 @@ void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, 
                      bool peer = false, int sms = 148, const mpk::SmallTable<mpk::kSmallMaxTiles>* small = nullptr,
                      int kind = PROG_DYNAMIC, mpk::Sched* sched = nullptr) {
   if (kind == PROG_SMALL && small && !trace && !gsync) {
+    // programmatic dependent launch (opts.pdl) from kPdlMinBytes: the kernel
+    // waits on griddepcontrol before any memory access, so stream order holds
+    uint64_t bytes = 0;
+    for (unsigned i = 0; i < ntiles; ++i) bytes += small->len[i];
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(ntiles);
+    lc.blockDim = dim3(256);
+    lc.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = o_in.pdl && bytes >= kPdlMinBytes ? 1 : 0;
     if (ntiles <= mpk::kSmallTilesLo) {
       mpk::SmallTable<mpk::kSmallTilesLo> lo;
       std::copy(small->src, small->src + ntiles, lo.src);
       std::copy(small->dst, small->dst + ntiles, lo.dst);
       std::copy(small->len, small->len + ntiles, lo.len);
-      mpk::small_copy_kernel<4, mpk::kSmallTilesLo><<<ntiles, 256, 0, s>>>(lo);
+      CK(cudaLaunchKernelEx(&lc, mpk::small_copy_kernel<4, mpk::kSmallTilesLo>, lo));
     } else {
-      mpk::small_copy_kernel<4, mpk::kSmallMaxTiles><<<ntiles, 256, 0, s>>>(*small);
+      CK(cudaLaunchKernelEx(&lc, mpk::small_copy_kernel<4, mpk::kSmallMaxTiles>, *small));
     }
-    CK(cudaGetLastError());
     return;
   }
   mp_engine_opts o = o_in;
@@ -181,6 +196,7 @@ struct Program {
   bool peer = false;     // some tile reads or writes another GPU's memory
   int kind = PROG_DYNAMIC;                 // ProgKind
   std::shared_ptr<mpk::SmallTable<mpk::kSmallMaxTiles>> small;  // PROG_SMALL: the table as kernel params
+  uint64_t bytes = 0;    // PROG_SMALL: bytes the table moves
 };
 
 // Hash of a cache key (raw bytes: pointers, sizes, devices, config; up to

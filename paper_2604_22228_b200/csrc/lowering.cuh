@@ -575,12 +575,15 @@ class Lowering {
       flat.resize(pr.ntiles);
       if (pr.kind == PROG_SMALL) {
         auto sm = std::make_shared<mpk::SmallTable<mpk::kSmallMaxTiles>>();
+        uint64_t bytes = 0;
         for (size_t i = 0; i < flat.size(); ++i) {
           sm->src[i] = flat[i].src;
           sm->dst[i] = flat[i].dst;
           sm->len[i] = (uint32_t)flat[i].len;
+          bytes += flat[i].len;
         }
         e_->progs.back().small = sm;
+        e_->progs.back().bytes = bytes;
       }
     }
     // A pageable-memory cudaMemcpy may return before its DMA reaches the

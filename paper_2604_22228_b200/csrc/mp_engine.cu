@@ -98,6 +98,21 @@ void enqueue_group(mp_ctx* ctx, Entry* e, cudaStream_t origin) {
   CK(cudaStreamWaitEvent(origin, j, 0));
 }
 
+// A cached single send whose whole program is ONE small-message kernel of
+// kPdlMinBytes..small_max_bytes on the caller's device replays as a direct
+// programmatic-dependent launch of that kernel instead of its one-node graph
+// (opts.pdl): back-to-back graph launches retire in 2.048 us quanta — two
+// (4.1 us) from ~1 MiB — while PDL launches overlap the next launch's
+// processing with the running kernel: 1-4 MiB sends 4.1 -> 2.7-3.6 us
+// (tools/exp_pdl.py, two boxes).  Below ~512 KiB the graph replay often
+// takes one quantum and its host path is cheaper, so it stays.  The graph is still
+// captured and instantiated (lifecycle phases; pdl = 0 replays it).
+bool pdl_replay(const mp_ctx* ctx, const Entry* e) {
+  return ctx->opts.pdl && !ctx->group && e->ce.empty() && e->progs.size() == 1 &&
+         e->progs[0].phys == e->src_phys && e->progs[0].kind == PROG_SMALL && e->progs[0].small &&
+         e->progs[0].bytes >= kPdlMinBytes;
+}
+
 void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr = nullptr) {
   if (ctx->group) {
     enqueue_group(ctx, e, origin);
@@ -458,6 +473,7 @@ int mp_ctx_create(int32_t n_logical, const int32_t* device_map, mp_ctx** out) {
   ctx->opts.tma_block = 32768;
   ctx->opts.sched = MP_SCHED_AUTO;
   ctx->opts.small_max_bytes = kSmallMaxBytes;
+  ctx->opts.pdl = 1;
   std::map<int, int> phys_of;
   for (int i = 0; i < n_logical; ++i) {
     int ord = device_map[i];
@@ -585,6 +601,7 @@ int mp_ctx_set_engine(mp_ctx* ctx, const mp_engine_opts* o) {
   if (o->sched != MP_SCHED_AUTO && o->sched != MP_SCHED_DYNAMIC) return fail(MP_ERR_VALUE, "unknown sched");
   if (o->small_max_bytes < 0 || o->small_max_bytes > (int64_t)1 << 31)
     return fail(MP_ERR_VALUE, "small_max_bytes must be in [0, 2^31]");
+  if (o->pdl < 0 || o->pdl > 1 || o->reserved != 0) return fail(MP_ERR_VALUE, "pdl must be 0 or 1");
   std::lock_guard<std::mutex> lk(ctx->mu);
   clear_cache(ctx);
   ctx->opts = *o;
@@ -651,7 +668,7 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
   if (ctx->have_last && ctx->last_stream != stream) CK(cudaStreamWaitEvent(user, ctx->last_done, 0));
   double t_launch = now_us();
   bool timing = !cfg->graph_mode && ctx->kernel_timing;
-  if (cfg->graph_mode && e->graph) {
+  if (cfg->graph_mode && e->graph && !pdl_replay(ctx, e)) {
     CK(cudaGraphLaunch(e->exec, user));
     st.ce_copies = (int)e->ce.size();
   } else {

@@ -461,6 +461,18 @@ struct TmaEngine {
 // all its 16-byte loads before any store, and there is no shared memory, no
 // barrier, no claim and no exit protocol.  Used for static tables of direct
 // tiles only (no flags, no host memory), one tile per CTA.
+//
+// Programmatic dependent launch: the "slots" are a property of ordinary
+// stream-ordered launches (one-kernel graph replays and plain launches
+// alike retire in 2.048 us quanta on B200).  Launched with programmatic
+// stream serialization (engine option pdl) the next send's kernel is
+// processed while this one runs and back-to-back sends cost ~1.9 us up to
+// 2 MiB (tools/pdl_probe.cu).  Stream order is kept on the device:
+// griddepcontrol.wait (before ANY global access) returns once the previous
+// grid has completed and its memory is visible — a no-op for a normal
+// launch — and each CTA allows the dependent launch only after its stores
+// are issued (an early trigger leaves the dependent's waiting CTAs resident
+// beside a long body: 4 MiB 5.9 vs 2.5 us).
 // ---------------------------------------------------------------------------
 constexpr unsigned kSmallMaxTiles = 148;
 template <unsigned N>
@@ -473,11 +485,15 @@ struct SmallTable {
 // 16 tiles (messages <= 64 KiB at 4 KiB tiles) use a 320-byte block.
 constexpr unsigned kSmallTilesLo = 16;
 
-template <int V, unsigned N>
-__global__ void __launch_bounds__(256) small_copy_kernel(const __grid_constant__ SmallTable<N> tab) {
-  const uint8_t* src = (const uint8_t*)tab.src[blockIdx.x];
-  uint8_t* dst = (uint8_t*)tab.dst[blockIdx.x];
-  const uint32_t len = tab.len[blockIdx.x];
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <int V>
+__device__ __forceinline__ void small_copy_body(uint64_t src_addr, uint64_t dst_addr, uint32_t len) {
+  const uint8_t* src = (const uint8_t*)src_addr;
+  uint8_t* dst = (uint8_t*)dst_addr;
   const uint32_t tid = threadIdx.x, nt = blockDim.x;
   if ((((uintptr_t)src ^ (uintptr_t)dst) & 15u) != 0) {
     copy_range<4, false>(src, dst, len);
@@ -504,6 +520,13 @@ __global__ void __launch_bounds__(256) small_copy_kernel(const __grid_constant__
   }
   if (hv) dst[tid] = hb;
   if (tv) dst[tail_at + tid] = tb;
+}
+
+template <int V, unsigned N>
+__global__ void __launch_bounds__(256) small_copy_kernel(const __grid_constant__ SmallTable<N> tab) {
+  griddep_wait();
+  small_copy_body<V>(tab.src[blockIdx.x], tab.dst[blockIdx.x], tab.len[blockIdx.x]);
+  griddep_launch_dependents();
 }
 
 // Time base of a traced send: %globaltimer at the fork point of this device.

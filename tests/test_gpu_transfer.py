@@ -378,3 +378,31 @@ def test_streamed_dynamic_tables_match_graph_replays():
         rates[graph] = e0.elapsed_time(e1)
     assert rates[False] < 1.25 * rates[True], rates
     eng.close()
+
+
+@pytest.mark.parametrize("pdl", [False, True])
+def test_chained_sends_keep_stream_order(pdl):
+    """Back-to-back sends where each reads what the previous one wrote
+    (a -> b, then b -> c, with a rewritten in between): with programmatic
+    dependent launch the next kernel may start early, so its
+    griddepcontrol.wait must order every access after the previous send."""
+    from paper_2604_22228_b200 import Engine, PathConfig
+    eng = Engine.loopback(2)
+    eng.configure(pdl=pdl)
+    cfg = PathConfig(max_chunks=1, graph_mode=True)
+    for n in (4096 + 5, 65536, (1 << 20) + 3, 3 << 20):
+        a = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+        b = torch.zeros_like(a)
+        c = torch.zeros_like(a)
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            for r in range(40):
+                a.fill_(r)
+                eng.send(a, b, n, cfg, stream=s, src_dev=0, dst_dev=1)
+                eng.send(b, c, n, cfg, stream=s, src_dev=0, dst_dev=1)
+                eng.send(c, a, n, cfg, stream=s, src_dev=0, dst_dev=1)
+                eng.send(a, b, n, cfg, stream=s, src_dev=0, dst_dev=1)
+        s.synchronize()
+        assert eng.stats().kernel.startswith("mpk::small_copy_kernel")
+        assert bool((b == 39).all()) and bool((c == 39).all())
+    eng.close()

@@ -17,12 +17,15 @@ def fmt(x):
 
 
 rows = {r["bytes"]: r for r in d["sweep"]}
-print("| bytes | CE single | SM single | direct+host k=8 (graph) | tuned |")
-print("|---|---|---|---|---|")
+prep = "sm_single_prepared" in d["sweep"][0]
+print("| bytes | CE single | SM single |" + (" SM single, prepared |" if prep else "")
+      + " direct+host k=8 (graph) | tuned |")
+print("|---|---|---|---|---|" + ("---|" if prep else ""))
 for b in (4 * KiB, 64 * KiB, MiB, 4 * MiB, 16 * MiB, 32 * MiB, 128 * MiB, 512 * MiB):
     r = rows[b]
     print(f"| {label(b)} | {fmt(r['ce_single'])} | {fmt(r['sm_single'])} | "
-          f"{fmt(r['multi_graph'])} | {fmt(r['tuned'])} |")
+          + (f"{fmt(r['sm_single_prepared'])} | " if prep else "")
+          + f"{fmt(r['multi_graph'])} | {fmt(r['tuned'])} |")
 w = d.get("windows")
 if w:
     print()
