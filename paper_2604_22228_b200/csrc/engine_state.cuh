@@ -128,9 +128,20 @@ void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, 
   if (smem > 48 * 1024) allow_smem(fn, smem);
   mpk::GroupSync g{};
   if (gsync) g = *gsync;
-  fn<<<grid, o.threads, smem, s>>>(tiles, ntiles, ctl, (unsigned)o.tma_stages, (unsigned)o.tma_block,
-                                   nstatic, trace, g, sched);
-  CK(cudaGetLastError());
+  // static tables (one tile per CTA, no waits, no control block) launch with
+  // programmatic dependent launch like the small-message kernel
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(o.threads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = o_in.pdl >= 2 && kind != PROG_DYNAMIC && !trace && !gsync ? 1 : 0;
+  CK(cudaLaunchKernelEx(&lc, fn, tiles, ntiles, ctl, (unsigned)o.tma_stages, (unsigned)o.tma_block,
+                        nstatic, trace, g, sched));
 }
 
 double now_us() {

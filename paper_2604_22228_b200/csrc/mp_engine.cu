@@ -108,9 +108,12 @@ void enqueue_group(mp_ctx* ctx, Entry* e, cudaStream_t origin) {
 // takes one quantum and its host path is cheaper, so it stays.  The graph is still
 // captured and instantiated (lifecycle phases; pdl = 0 replays it).
 bool pdl_replay(const mp_ctx* ctx, const Entry* e) {
-  return ctx->opts.pdl && !ctx->group && e->ce.empty() && e->progs.size() == 1 &&
-         e->progs[0].phys == e->src_phys && e->progs[0].kind == PROG_SMALL && e->progs[0].small &&
-         e->progs[0].bytes >= kPdlMinBytes;
+  if (!ctx->opts.pdl || ctx->group || !e->ce.empty() || e->progs.size() != 1 ||
+      e->progs[0].phys != e->src_phys)
+    return false;
+  const Program& pr = e->progs[0];
+  if (pr.kind == PROG_SMALL) return pr.small && pr.bytes >= kPdlMinBytes;
+  return pr.kind == PROG_STATIC_TMA && ctx->opts.pdl >= 2;
 }
 
 void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr = nullptr) {
@@ -601,7 +604,7 @@ int mp_ctx_set_engine(mp_ctx* ctx, const mp_engine_opts* o) {
   if (o->sched != MP_SCHED_AUTO && o->sched != MP_SCHED_DYNAMIC) return fail(MP_ERR_VALUE, "unknown sched");
   if (o->small_max_bytes < 0 || o->small_max_bytes > (int64_t)1 << 31)
     return fail(MP_ERR_VALUE, "small_max_bytes must be in [0, 2^31]");
-  if (o->pdl < 0 || o->pdl > 1 || o->reserved != 0) return fail(MP_ERR_VALUE, "pdl must be 0 or 1");
+  if (o->pdl < 0 || o->pdl > 2 || o->reserved != 0) return fail(MP_ERR_VALUE, "pdl must be 0, 1 or 2");
   std::lock_guard<std::mutex> lk(ctx->mu);
   clear_cache(ctx);
   ctx->opts = *o;

@@ -542,6 +542,9 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
                                                        unsigned nstatic,
                                                        unsigned long long* trace,
                                                        GroupSync gsync, Sched* sched) {
+  // programmatic dependent launch (static tables, engine option pdl): no
+  // global access before the previous grid has completed (a no-op otherwise)
+  griddep_wait();
   // Tiles [0, nstatic) (a prefix with no flag waits, nstatic <= gridDim.x) are
   // taken by CTA blockIdx.x without a claim; the rest are claimed dynamically.
   // A fully static table (nstatic == ntiles: one tile per CTA, no waits) runs
@@ -681,6 +684,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       group_done(gsync);
     }
   }
+  griddep_launch_dependents();
 }
 
 // Receiver side of a group transfer: wait until `expected` bytes have landed

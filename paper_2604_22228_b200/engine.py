@@ -116,7 +116,7 @@ class Engine:
                   copy: str | None = None, unroll: int | None = None,
                   tma_stages: int | None = None, tma_block: int | None = None,
                   tma_peer: bool | None = None, sched: str | None = None,
-                  small_max_bytes: int | None = None, pdl: bool | None = None) -> None:
+                  small_max_bytes: int | None = None, pdl: int | None = None) -> None:
         """Pick the copy mechanism per path type and the SM-kernel shape.
         `sched`: "auto" (static one-tile-per-CTA tables when no tile waits or
         touches host memory) or "dynamic" (atomic tile claims always)."""
@@ -125,7 +125,7 @@ class Engine:
         if small_max_bytes is not None:
             o.small_max_bytes = small_max_bytes
         if pdl is not None:
-            o.pdl = int(bool(pdl))
+            o.pdl = int(pdl)
         if sched is not None:
             o.sched = {"auto": _lib.MP_SCHED_AUTO, "dynamic": _lib.MP_SCHED_DYNAMIC}[sched]
         if tma_peer is not None:
