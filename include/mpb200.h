@@ -197,14 +197,15 @@ typedef struct {
   int32_t sched;             /* MP_SCHED_*: tile scheduling of the SM kernel */
   int64_t small_max_bytes;   /* static direct tables up to this size run the
                                 one-launch-slot small-message kernel (0 = off) */
-  int32_t pdl;               /* 1 (default): a send whose program is ONE
-                                small-message kernel of >= 1 MiB launches
-                                it with programmatic dependent launch (the kernel
-                                waits on griddepcontrol before touching
-                                memory), graph mode included: B200 retires
+  int32_t pdl;               /* programmatic dependent launch of sends whose
+                                program is ONE kernel (the kernel waits on
+                                griddepcontrol before touching memory),
+                                graph mode included: B200 retires
                                 back-to-back one-kernel graph launches in
                                 2.048 us quanta, PDL launches do not
-                                (tools/pdl_probe.cu); 0: graph replay   */
+                                (tools/pdl_probe.cu).  0: off (graph
+                                replay); 1: small-message kernel >= 1 MiB;
+                                2 (default): also static TMA tables      */
   int32_t reserved;          /* 0 */
 } mp_engine_opts;
 

@@ -98,14 +98,16 @@ void enqueue_group(mp_ctx* ctx, Entry* e, cudaStream_t origin) {
   CK(cudaStreamWaitEvent(origin, j, 0));
 }
 
-// A cached single send whose whole program is ONE small-message kernel of
-// kPdlMinBytes..small_max_bytes on the caller's device replays as a direct
-// programmatic-dependent launch of that kernel instead of its one-node graph
-// (opts.pdl): back-to-back graph launches retire in 2.048 us quanta — two
-// (4.1 us) from ~1 MiB — while PDL launches overlap the next launch's
-// processing with the running kernel: 1-4 MiB sends 4.1 -> 2.7-3.6 us
-// (tools/exp_pdl.py, two boxes).  Below ~512 KiB the graph replay often
-// takes one quantum and its host path is cheaper, so it stays.  The graph is still
+// A cached single send whose whole program is ONE kernel on the caller's
+// device — the small-message kernel from kPdlMinBytes (opts.pdl >= 1) or a
+// static one-tile-per-CTA TMA table (opts.pdl = 2, the default) — replays as
+// a direct programmatic-dependent launch of that kernel instead of its
+// one-node graph: back-to-back graph launches retire in 2.048 us quanta
+// (1-4 MiB: 4.1 us, 16 MiB: 8.2 us) while PDL launches overlap the next
+// launch's processing with the running kernel: 1-4 MiB 4.1 -> 2.5-3.4 us,
+// 8 MiB 6.1 -> 3.8, 16 MiB 8.2 -> 5.4, 32 MiB 10.2 -> 8.0
+// (tools/exp_pdl.py).  Below ~512 KiB the graph replay often takes one
+// quantum and its host path is cheaper, so it stays.  The graph is still
 // captured and instantiated (lifecycle phases; pdl = 0 replays it).
 bool pdl_replay(const mp_ctx* ctx, const Entry* e) {
   if (!ctx->opts.pdl || ctx->group || !e->ce.empty() || e->progs.size() != 1 ||
@@ -476,7 +478,7 @@ int mp_ctx_create(int32_t n_logical, const int32_t* device_map, mp_ctx** out) {
   ctx->opts.tma_block = 32768;
   ctx->opts.sched = MP_SCHED_AUTO;
   ctx->opts.small_max_bytes = kSmallMaxBytes;
-  ctx->opts.pdl = 1;
+  ctx->opts.pdl = 2;
   std::map<int, int> phys_of;
   for (int i = 0; i < n_logical; ++i) {
     int ord = device_map[i];
