@@ -8,11 +8,11 @@ import torch  # noqa: E402
 
 from paper_2604_22228_b200 import Engine, PathConfig  # noqa: E402
 
-sizes = [1 << 20, 4 << 20, 8 << 20, 16 << 20, 32 << 20, 64 << 20]
+sizes = [4 << 10, 64 << 10, 1 << 20, 4 << 20, 8 << 20, 16 << 20, 32 << 20, 64 << 20]
 big = torch.randint(0, 256, (max(sizes),), dtype=torch.uint8, device="cuda")
 out = torch.empty_like(big)
 s = torch.cuda.Stream()
-for pdl in (1, 2, 1, 2):
+for pdl in (0, 2, 0, 2):
     eng = Engine.loopback(2)
     eng.configure(pdl=pdl)
     row = []
