@@ -205,7 +205,8 @@ typedef struct {
                                 2.048 us quanta, PDL launches do not
                                 (tools/pdl_probe.cu).  0: off (graph
                                 replay); 1: small-message kernel >= 1 MiB;
-                                2 (default): also static TMA tables      */
+                                2: also static TMA tables; 3 (default):
+                                also dynamic tables                      */
   int32_t reserved;          /* 0 */
 } mp_engine_opts;
 

@@ -139,7 +139,7 @@ void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, 
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
-  lc.numAttrs = o_in.pdl >= 2 && kind != PROG_DYNAMIC && !trace && !gsync ? 1 : 0;
+  lc.numAttrs = (o_in.pdl >= 3 || (o_in.pdl >= 2 && kind != PROG_DYNAMIC)) && !trace && !gsync ? 1 : 0;
   CK(cudaLaunchKernelEx(&lc, fn, tiles, ntiles, ctl, (unsigned)o.tma_stages, (unsigned)o.tma_block,
                         nstatic, trace, g, sched));
 }

@@ -380,7 +380,7 @@ def test_streamed_dynamic_tables_match_graph_replays():
     eng.close()
 
 
-@pytest.mark.parametrize("pdl", [0, 1, 2])
+@pytest.mark.parametrize("pdl", [0, 1, 2, 3])
 def test_chained_sends_keep_stream_order(pdl):
     """Back-to-back sends where each reads what the previous one wrote
     (a -> b, then b -> c, with a rewritten in between): with programmatic
@@ -390,7 +390,7 @@ def test_chained_sends_keep_stream_order(pdl):
     eng = Engine.loopback(2)
     eng.configure(pdl=pdl)
     cfg = PathConfig(max_chunks=1, graph_mode=True)
-    for n in (4096 + 5, 65536, (1 << 20) + 3, 3 << 20, (16 << 20) + 7):
+    for n in (4096 + 5, 65536, (1 << 20) + 3, 3 << 20, (16 << 20) + 7, (160 << 20) + 9):
         a = torch.empty(n, dtype=torch.uint8, device="cuda:0")
         b = torch.zeros_like(a)
         c = torch.zeros_like(a)
@@ -403,7 +403,8 @@ def test_chained_sends_keep_stream_order(pdl):
                 eng.send(c, a, n, cfg, stream=s, src_dev=0, dst_dev=1)
                 eng.send(a, b, n, cfg, stream=s, src_dev=0, dst_dev=1)
         s.synchronize()
-        assert eng.stats().kernel.startswith("mpk::small_copy_kernel" if n < (4 << 20)
-                                             else "mpk::transfer_kernel<1")
+        want = ("mpk::small_copy_kernel" if n < (4 << 20) else
+                "mpk::transfer_kernel<1" if n < (64 << 20) else "mpk::transfer_kernel<0")
+        assert eng.stats().kernel.startswith(want)
         assert bool((b == 39).all()) and bool((c == 39).all())
     eng.close()
