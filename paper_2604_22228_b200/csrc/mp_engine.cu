@@ -998,11 +998,15 @@ int mp_kernel_bench(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int3
   Phys& S = ctx->phys[e->src_phys];
   CK(cudaSetDevice(S.ordinal));
   CK(cudaDeviceSynchronize());
-  launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
+  // ordinary launches: the kernel's own duration, launch gap included (PDL
+  // would overlap each launch with the previous kernel's tail)
+  mp_engine_opts o = ctx->opts;
+  o.pdl = 0;
+  launch_transfer(o, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
                   nullptr, pr->peer, S.sms, pr->small.get(), pr->kind, pr->d_sched);  // warm
   CK(cudaEventRecord(S.kt0, S.kstream));
   for (int i = 0; i < reps; ++i)
-    launch_transfer(ctx->opts, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
+    launch_transfer(o, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
                     nullptr, pr->peer, S.sms, pr->small.get(), pr->kind, pr->d_sched);
   CK(cudaEventRecord(S.kt1, S.kstream));
   CK(cudaEventSynchronize(S.kt1));
