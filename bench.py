@@ -184,8 +184,13 @@ def run_reference(args, rank):
 
     from oracle import planner as op
     from oracle import transfer as ot
-    topo = op.parse_topology(loopback_topo_text(3000e9, 50e9))
-    paths = op.plan_paths(topo, 0, 1, 1, True)
+    world = max(1, args.gpus)
+    if world > 1:  # the N > 1 arm's workload: direct + (N - 2) GPU relays, no host path
+        topo = op.parse_topology(loopback_topo_text(900e9, 64e9, n=world))
+        paths = op.plan_paths(topo, 0, 1, world - 1, False)
+    else:
+        topo = op.parse_topology(loopback_topo_text(3000e9, 50e9))
+        paths = op.plan_paths(topo, 0, 1, 1, True)
     src = ot.pattern(size)
     dst = np.empty_like(src)
     for _ in range(args.warmup):
@@ -198,17 +203,29 @@ def run_reference(args, rank):
     dt = time.perf_counter() - t0
     assert np.array_equal(src, dst)
     gbs = args.steps * size / dt / 1e9
-    sample = f"{args.steps} x {size} B messages, direct+host plan, {threads} threads, numpy"
+    sample = (f"{args.steps} x {size} B messages, "
+              f"{'direct+host' if world == 1 else f'direct + {world - 2} relays'} plan, "
+              f"{threads} threads, numpy")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak" if world == 1 else "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": workload_config(args),
+        "config": workload_config(args) if world == 1 else group_config(args, world),
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": sample, **cpu_info()},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def group_config(args, world):
+    """config of the N > 1 arm (run_group); the reference arm mirrors it."""
+    return {"workload": f"GPU0->GPU1 {args.size} B messages, direct + {world - 2} GPU "
+                        f"relays, max_chunks {args.chunks}, multi-process group mode "
+                        "(CUDA IPC), cached graphs", "msg_bytes": args.size,
+            "window": args.window, "relays": world - 2, "parallelism": f"n{world}",
+            "l2": "inputs larger than L2"}
 
 
 def loopback_topo_text(link_bw, host_bw, n=2):
@@ -840,11 +857,7 @@ def run_group(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded random bytes)",
-            "config": {"workload": f"GPU0->GPU1 {size} B messages, direct + {world - 2} GPU "
-                                   f"relays, max_chunks {args.chunks}, multi-process group mode "
-                                   "(CUDA IPC), cached graphs", "msg_bytes": size,
-                       "window": W, "relays": world - 2, "parallelism": f"n{world}",
-                       "l2": "inputs larger than L2"},
+            "config": group_config(args, world),
             "roofline": {"bound": "nvlink", "achieved": value, "peak": peer_peak,
                          "unit": "GB/s", "frac": value / peer_peak, "traffic": None,
                          "peak_kind": "B200_PROFILING.md measured peer copy (900 nominal)",
