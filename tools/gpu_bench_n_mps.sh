@@ -7,7 +7,7 @@ export CUDA_MPS_PIPE_DIRECTORY=/tmp/mps_pipe CUDA_MPS_LOG_DIRECTORY=/tmp/mps_log
 mkdir -p $CUDA_MPS_PIPE_DIRECTORY $CUDA_MPS_LOG_DIRECTORY
 nvidia-cuda-mps-control -d && echo "MPS started"
 python paper_2604_22228_b200/build.py > gpurun_out/build.log 2>&1 || exit 1
-for N in 2 3 4; do
+for N in ${NS:-2 3 4}; do
 # each rank gets 1/N of the SMs (MPS execution-resource provisioning): a
 # relay rank's flag-waiting CTAs then cannot occupy the SMs the sender's
 # CTAs need, as on separate GPUs
