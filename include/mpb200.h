@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define MP_ABI_VERSION 2
+#define MP_ABI_VERSION 3
 
 /* ---- status codes -------------------------------------------------------- */
 #define MP_OK 0
@@ -207,7 +207,15 @@ typedef struct {
                                 replay); 1: small-message kernel >= 1 MiB;
                                 2: also static TMA tables; 3 (default):
                                 also dynamic tables                      */
-  int32_t reserved;          /* 0 */
+  int32_t wait_timeout_ms;   /* limit of a relay-flag / group-barrier wait
+                                (0 = 4000).  A wait that times out skips
+                                its tile (staging is never copied
+                                unsignalled) and makes the error sticky:
+                                every later mp_send / mp_send_many /
+                                mp_wait / mp_group_send fails until
+                                mp_sync reports and clears it            */
+  int32_t fault_inject;      /* testing only: 1 = the first staged chunk's
+                                hop1 tiles never signal (forces a timeout) */
 } mp_engine_opts;
 
 /* ---- errors / version ---------------------------------------------------- */
@@ -363,6 +371,9 @@ int mp_last_plan(const mp_ctx* ctx, mp_path* paths, int32_t paths_cap,
                  int32_t* n_paths, mp_chunk* chunks, int32_t chunks_cap,
                  int32_t* n_chunks);
 int mp_cache_clear(mp_ctx* ctx);
+/* Wait for every transfer of the context.  If a wait timed out (see
+ * mp_engine_opts.wait_timeout_ms) it fails with the error and clears it:
+ * flag arrays and control blocks are re-zeroed, later sends run again. */
 int mp_sync(mp_ctx* ctx);
 
 /* Per-path bandwidth probe: times `iters` copies of `bytes` over each path

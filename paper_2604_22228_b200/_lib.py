@@ -1,7 +1,10 @@
 """ctypes binding of the in-tree C ABI (include/mpb200.h, libmpb200.so).
 
 There is no Python fallback: if the library is missing the import fails with
-a message telling how to build it.  Every call returns a status; `check`
+a message telling how to build it (the one exception is the build command
+itself, `python -m paper_2604_22228_b200.build`, which must import the
+package before the library exists: then `lib` is None and the package
+exports nothing).  Every call returns a status; `check`
 re-raises failures as the reference's exception classes with the message
 text produced by the C++ side (which reproduces the reference wording).
 """
@@ -10,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmpb200.so")
@@ -113,7 +117,8 @@ class mp_engine_opts(C.Structure):
                 ("sm_min_bytes", C.c_int64), ("unroll", C.c_int32), ("tma_stages", C.c_int32),
                 ("tma_block", C.c_int32), ("host_engine", C.c_int32), ("tma_peer", C.c_int32),
                 ("sched", C.c_int32), ("small_max_bytes", C.c_int64),
-                ("pdl", C.c_int32), ("reserved", C.c_int32)]
+                ("pdl", C.c_int32), ("wait_timeout_ms", C.c_int32),
+                ("fault_inject", C.c_int32)]
 
 
 P = C.POINTER
@@ -196,7 +201,7 @@ def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
             f"{LIB_PATH} is missing: build the sm_100a engine first "
-            "(python -m paper_2604_22228_b200.build). There is no Python fallback.")
+            "(python -m paper_2604_22228_b200.build, or python paper_2604_22228_b200/build.py). There is no Python fallback.")
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
@@ -205,7 +210,13 @@ def _load() -> C.CDLL:
     return lib
 
 
-lib = _load()
+def _building() -> bool:
+    """True while `python -m paper_2604_22228_b200.build` imports the package."""
+    a = getattr(sys, "orig_argv", [])
+    return any(x == "-m" and y == f"{__package__}.build" for x, y in zip(a, a[1:]))
+
+
+lib = None if _building() else _load()
 
 
 class EngineError(RuntimeError):

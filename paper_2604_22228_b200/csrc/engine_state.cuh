@@ -162,6 +162,7 @@ struct Phys {
   int ordinal = 0;
   int sms = 148;
   mpk::Ctl* ctl = nullptr;               // transfer-kernel control block
+  unsigned* herr_dev = nullptr;          // device view of this device's sticky error word
   cudaStream_t kstream = nullptr;        // SM transfer-kernel stream
   cudaStream_t capture = nullptr;        // graph-capture origin
   std::vector<cudaStream_t> lanes;       // copy-engine lane streams
@@ -278,6 +279,10 @@ struct mp_ctx {
   mp_engine_opts opts{};
   uint8_t* host_stage = nullptr;
   size_t host_cap = 0;
+  // sticky wait-timeout codes, one per physical device, in mapped pinned
+  // memory: kernels write them (mpk::raise_error), every send reads them
+  // with a plain load before it enqueues anything; mp_sync clears them
+  unsigned* herr = nullptr;
   std::list<Entry*> lru;  // least recent first
   std::unordered_map<std::string, std::list<Entry*>::iterator, KeyHash> index;
   mp_send_stats stats{};

@@ -161,6 +161,15 @@ class Lowering {
   uint64_t host_cursor_ = 0;            // shared pinned arena
   uint32_t node_ = 0;  // logical node id of a chunk's first hop (graph.py:97-117), global
   int lane_next_ = 0;
+  bool faulted_ = false;  // opts.fault_inject: one staged chunk's hop1 already muted
+
+  // Testing only (opts.fault_inject = 1): the first staged chunk's hop1
+  // tiles never signal, so its hop2 wait times out (sticky-error tests).
+  uint32_t* hop1_signal(uint32_t* flag) {
+    if (o_.fault_inject != 1 || faulted_) return flag;
+    faulted_ = true;
+    return nullptr;
+  }
 
   int phys_of(int logical) const { return ctx_->logi[logical].phys; }
   int new_event(int phys) {
@@ -417,7 +426,7 @@ class Lowering {
     const uint64_t t1 = tile_for(sp, pi.bytes);
     const uint64_t t2 = tile_for(rp, pi.bytes);  // 64 KiB on the LDG/STG kernel (+4% vs auto)
     mpk::Tile h1{};
-    h1.signal = L.flags + g;
+    h1.signal = hop1_signal(L.flags + g);
     h1.node = n_a;
     const uint64_t r2 = 2 * (uint64_t)ch.seq;
     append_tiles(tiles_[sp], order(t, r2), s0 + ch.offset, (uint64_t)(uintptr_t)stage, ch.length, t1, h1);
@@ -448,7 +457,7 @@ class Lowering {
     host_cursor_ += ch.length;
     const uint64_t th = std::min<uint64_t>(auto_tile_bytes(ctx_, pi.bytes, ctx_->phys[sp].sms), kHostTileBytes);
     mpk::Tile h1{};
-    h1.signal = L.flags + g;
+    h1.signal = hop1_signal(L.flags + g);
     h1.node = n_a;
     append_tiles(tiles_[sp], (uint64_t)t, s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
     mpk::Tile h2{};

@@ -290,7 +290,10 @@ Entry* lookup_entry(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int 
     ctx->lru.pop_front();
     ctx->index.erase(old->key);
     CK(cudaSetDevice(ctx->phys[old->src_phys].ordinal));
-    CK(cudaStreamSynchronize(user));  // old graph may still be replaying
+    // the old entry may still be replaying on `user` or on the stream of the
+    // previous send (which `user` has not been made to wait for yet)
+    CK(cudaStreamSynchronize(user));
+    if (ctx->have_last) CK(cudaEventSynchronize(ctx->last_done));
     destroy_entry(ctx, old);
     st.cache_evictions++;
   }
@@ -299,6 +302,9 @@ Entry* lookup_entry(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int 
   return e;
 }
 
+
+// Group mode: tile size of relay hops, agreed by construction across ranks.
+constexpr uint64_t kGroupRelayTileBytes = 64 << 10;
 
 // Serialized CUDA-IPC handles of one rank's group resource block.
 struct GroupBlob {
@@ -361,7 +367,10 @@ Entry* build_group_entry(mp_ctx* ctx, const std::string& key, const void* src, u
     stage_off[p] += ch.length;
     const size_t cap = k == me ? G->stage_cap : G->peer_stage_cap[k];
     if (stage_off[p] > cap) throw Error{MP_ERR_STATE, "group staging arena too small for the relay share"};
-    const uint64_t t1 = auto_tile_bytes(ctx, path_bytes[p], sms);
+    // relay tiles are cut identically on the sender (hop1 signals) and the
+    // relay rank (hop2 waits for that many signals): a size that depends on
+    // nothing rank-local (not the SM count, not the engine options)
+    const uint64_t t1 = kGroupRelayTileBytes;
     if (e->grole == 1) {
       uint8_t* stage = G->peer_stage[k] + so;
       mpk::Tile h1{};
@@ -432,6 +441,39 @@ uint64_t allocation_base(const void* p) {
   if (fn(&base, &sz, (unsigned long long)(uintptr_t)p) != 0)
     throw Error{MP_ERR_CUDA, "cuMemGetAddressRange failed"};
   return base;
+}
+
+const char* wait_what(unsigned code) {
+  static const char* what[] = {"wait", "relay flag wait", "group barrier wait", "receiver byte-count wait"};
+  return code <= 3 ? what[code] : what[0];
+}
+
+// A kernel's wait timed out since the last mp_sync: fail every later send
+// (the error word is in mapped host memory, so this is a plain load).
+void check_sticky(const mp_ctx* ctx) {
+  if (!ctx->herr) return;
+  for (size_t i = 0; i < ctx->phys.size(); ++i) {
+    const unsigned c = ((volatile const unsigned*)ctx->herr)[i];
+    if (c)
+      throw Error{MP_ERR_CUDA, std::string(wait_what(c)) + " timed out on device " +
+                                   std::to_string(ctx->phys[i].ordinal) +
+                                   ": a transfer was not delivered (its staged bytes were never copied); "
+                                   "mp_sync reports and clears the error"};
+  }
+}
+
+uint64_t timeout_ns(const mp_engine_opts& o) { return (uint64_t)o.wait_timeout_ms * 1000000ull; }
+
+// (Re)initialise a device's control block: zero counters and error word,
+// the host error word's device address and the wait limit.
+void init_ctl(mp_ctx* ctx, Phys& P) {
+  mpk::Ctl c{};
+  c.herr = P.herr_dev;
+  c.timeout_ns = timeout_ns(ctx->opts);
+  DeviceGuard g;
+  CK(cudaSetDevice(P.ordinal));
+  CK(cudaMemcpy(P.ctl, &c, sizeof c, cudaMemcpyHostToDevice));
+  CK(cudaDeviceSynchronize());  // lands before any launch on a non-blocking stream
 }
 
 }  // namespace
@@ -506,9 +548,6 @@ int mp_ctx_create(int32_t n_logical, const int32_t* device_map, mp_ctx** out) {
     CK(cudaGetDeviceProperties(&prop, P.ordinal));
     P.sms = prop.multiProcessorCount;
     CK(cudaMalloc(&P.ctl, sizeof(mpk::Ctl)));
-    CK(cudaMemset(P.ctl, 0, sizeof(mpk::Ctl)));
-    CK(cudaDeviceSynchronize());  // a legacy-stream memset is not ordered before
-                                  // launches on the non-blocking caller streams
     CK(cudaStreamCreateWithFlags(&P.kstream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&P.capture, cudaStreamNonBlocking));
     CK(cudaEventCreate(&P.kt0));
@@ -529,6 +568,12 @@ int mp_ctx_create(int32_t n_logical, const int32_t* device_map, mp_ctx** out) {
     }
   }
   CK(cudaSetDevice(ctx->phys[0].ordinal));
+  CK(cudaHostAlloc((void**)&ctx->herr, np * sizeof(unsigned), cudaHostAllocPortable | cudaHostAllocMapped));
+  for (int a = 0; a < np; ++a) {
+    ctx->herr[a] = 0u;
+    CK(cudaHostGetDevicePointer((void**)&ctx->phys[a].herr_dev, ctx->herr + a, 0));
+    init_ctl(ctx.get(), ctx->phys[a]);
+  }
   CK(cudaEventCreateWithFlags(&ctx->last_done, cudaEventDisableTiming));
   CK(cudaDeviceSynchronize());
   *out = ctx.release();
@@ -561,6 +606,7 @@ void mp_ctx_destroy(mp_ctx* ctx) {
     if (L.flags) cudaFree(L.flags);
   }
   if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+  if (ctx->herr) cudaFreeHost(ctx->herr);
   for (auto& P : ctx->phys) {
     cudaSetDevice(P.ordinal);
     for (auto s : P.lanes) cudaStreamDestroy(s);
@@ -608,10 +654,19 @@ int mp_ctx_set_engine(mp_ctx* ctx, const mp_engine_opts* o) {
   if (o->sched != MP_SCHED_AUTO && o->sched != MP_SCHED_DYNAMIC) return fail(MP_ERR_VALUE, "unknown sched");
   if (o->small_max_bytes < 0 || o->small_max_bytes > (int64_t)1 << 31)
     return fail(MP_ERR_VALUE, "small_max_bytes must be in [0, 2^31]");
-  if (o->pdl < 0 || o->pdl > 3 || o->reserved != 0) return fail(MP_ERR_VALUE, "pdl must be 0..3");
+  if (o->pdl < 0 || o->pdl > 3) return fail(MP_ERR_VALUE, "pdl must be 0..3");
+  if (o->wait_timeout_ms < 0) return fail(MP_ERR_VALUE, "wait_timeout_ms must be >= 0");
+  if (o->fault_inject < 0 || o->fault_inject > 1) return fail(MP_ERR_VALUE, "fault_inject must be 0 or 1");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g;
   clear_cache(ctx);
   ctx->opts = *o;
+  const unsigned long long lim = timeout_ns(*o);
+  for (auto& P : ctx->phys) {  // the wait limit lives in the control block
+    CK(cudaSetDevice(P.ordinal));
+    CK(cudaMemcpy(&P.ctl->timeout_ns, &lim, sizeof lim, cudaMemcpyHostToDevice));
+    CK(cudaDeviceSynchronize());
+  }
   return MP_OK;
   GUARD_END
 }
@@ -664,6 +719,7 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
   }
   if (size == 0) return fail(MP_ERR_CHUNK, "message size must be >= 1 byte, got 0");
   if (!src || !dst) return fail(MP_ERR_VALUE, "null buffer");
+  check_sticky(ctx);
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
   cudaStream_t user = (cudaStream_t)stream;
@@ -705,6 +761,7 @@ int mp_send_many(mp_ctx* ctx, const mp_xfer* xfers, int32_t n, const mp_config* 
   if (!ctx || !cfg || !xfers || n < 1 || n > 64) return fail(MP_ERR_VALUE, "need 1..64 transfers");
   if (!ctx->has_topo) return fail(MP_ERR_STATE, "context has no topology (mp_ctx_set_topology)");
   if (ctx->group) return fail(MP_ERR_STATE, "group context: use mp_group_send");
+  check_sticky(ctx);
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
   cudaStream_t user = (cudaStream_t)stream;
@@ -797,6 +854,7 @@ int mp_send_trace(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_
     return fail(MP_ERR_PLAN, "transfers run between accelerators");
   if (size == 0) return fail(MP_ERR_CHUNK, "message size must be >= 1 byte, got 0");
   if (!src || !dst) return fail(MP_ERR_VALUE, "null buffer");
+  check_sticky(ctx);
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
   mp_config c = *cfg;
@@ -897,6 +955,7 @@ int mp_send_trace(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_
 int mp_wait(mp_ctx* ctx, void* stream) {
   GUARD_BEGIN
   if (!ctx) return fail(MP_ERR_VALUE, "null argument");
+  check_sticky(ctx);
   std::lock_guard<std::mutex> lk(ctx->mu);
   if (ctx->have_last) CK(cudaStreamWaitEvent((cudaStream_t)stream, ctx->last_done, 0));
   return MP_OK;
@@ -936,21 +995,43 @@ int mp_cache_clear(mp_ctx* ctx) {
 int mp_sync(mp_ctx* ctx) {
   GUARD_BEGIN
   if (!ctx) return fail(MP_ERR_VALUE, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
+  unsigned code = 0;
+  int where = -1;
   for (auto& P : ctx->phys) {
     CK(cudaSetDevice(P.ordinal));
     CK(cudaDeviceSynchronize());
     mpk::Ctl c;
     CK(cudaMemcpy(&c, P.ctl, sizeof c, cudaMemcpyDeviceToHost));
-    if (c.error) {
-      CK(cudaMemset(P.ctl, 0, sizeof(mpk::Ctl)));
-      CK(cudaDeviceSynchronize());
-      static const char* what[] = {"", "relay flag wait", "group barrier wait", "receiver byte-count wait"};
-      return fail(MP_ERR_CUDA, std::string(c.error <= 3 ? what[c.error] : "wait") + " timed out on device " +
-                                   std::to_string(P.ordinal));
+    const unsigned h = ((volatile unsigned*)ctx->herr)[&P - ctx->phys.data()];
+    if ((c.error || h) && !code) {
+      code = c.error ? c.error : h;
+      where = P.ordinal;
     }
   }
-  return MP_OK;
+  if (!code) return MP_OK;
+  // Clear the error: a timed-out wait left its chunk's flag / pass counters
+  // (and a late hop1 signal may still have landed) — re-zero every flag
+  // array and control block so the next program starts from a clean state.
+  for (auto& L : ctx->logi)
+    if (L.phys >= 0 && L.flags) {
+      CK(cudaSetDevice(ctx->phys[L.phys].ordinal));
+      CK(cudaMemset(L.flags, 0, (size_t)L.flag_cap * 2 * sizeof(uint32_t)));
+    }
+  if (GroupState* G = ctx->group) {
+    CK(cudaSetDevice(ctx->phys[0].ordinal));
+    CK(cudaMemset(G->flags, 0, (size_t)G->flag_cap * 2 * sizeof(uint32_t)));
+    CK(cudaMemset(G->sync + 8, 0, 8));  // receiver byte counter
+  }
+  for (auto& P : ctx->phys) {
+    CK(cudaSetDevice(P.ordinal));
+    CK(cudaDeviceSynchronize());
+    ((volatile unsigned*)ctx->herr)[&P - ctx->phys.data()] = 0u;
+    init_ctl(ctx, P);
+  }
+  return fail(MP_ERR_CUDA, std::string(wait_what(code)) + " timed out on device " + std::to_string(where) +
+                               (ctx->group ? " (group barrier state may be inconsistent: recreate the group)" : ""));
   GUARD_END
 }
 
@@ -985,6 +1066,7 @@ int mp_kernel_bench(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int3
   if (src_dev < 0 || src_dev >= (int)ctx->logi.size() || dst_dev < 0 || dst_dev >= (int)ctx->logi.size())
     return fail(MP_ERR_PLAN, "transfers run between accelerators");
   if (!src || !dst || size == 0) return fail(MP_ERR_VALUE, "null buffer or empty message");
+  check_sticky(ctx);
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
   mp_config c = *cfg;
@@ -1310,6 +1392,7 @@ int mp_group_send(mp_ctx* ctx, const void* src, uint32_t src_align, void* dst, u
   if (G->rank == src_rank && !src) return fail(MP_ERR_VALUE, "the sender needs its source buffer");
   for (int q = 0; q < G->nranks; ++q)
     if (q != G->rank && !G->peer_sync[q]) return fail(MP_ERR_STATE, "group peers not imported");
+  check_sticky(ctx);
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
   cudaStream_t user = (cudaStream_t)stream;

@@ -65,8 +65,11 @@ struct __align__(16) Sched {
 struct __align__(16) Ctl {
   unsigned int work;     // next tile to claim
   unsigned int exit;     // CTAs finished
-  unsigned int error;    // 1 = a wait timed out
+  unsigned int error;    // non-zero: a wait timed out (1 relay flag, 2 group barrier, 3 receiver)
   unsigned int launches;
+  unsigned int* herr;    // the same code, in mapped pinned host memory: the host sees a
+                         // timeout with a plain load and fails every later send (sticky)
+  unsigned long long timeout_ns;  // flag / barrier wait limit (0: kWaitTimeoutNs)
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -154,6 +157,23 @@ __device__ __forceinline__ void copy_range(const uint8_t* __restrict__ src,
 
 constexpr uint64_t kWaitTimeoutNs = 4000000000ull;  // 4 s: never hang the GPU
 
+// A wait timed out: record the code on the device and in host memory (the
+// host checks the mapped word before every send, so the error is sticky
+// until mp_sync clears it).  The first error wins.
+__device__ __forceinline__ void raise_error(Ctl* ctl, unsigned code) {
+  if (atomicCAS(&ctl->error, 0u, code) == 0u && ctl->herr) {
+    *(volatile unsigned*)ctl->herr = code;
+    __threadfence_system();
+  }
+}
+
+// A wait gives up at the limit, or at once when another wait of this device
+// already failed (every later wait would time out behind it).
+__device__ __forceinline__ bool wait_expired(const Ctl* ctl, uint64_t t0) {
+  const uint64_t lim = ctl->timeout_ns ? ctl->timeout_ns : kWaitTimeoutNs;
+  return globaltimer() - t0 > lim || *(volatile const unsigned*)&ctl->error != 0u;
+}
+
 // ---------------------------------------------------------------------------
 // TMA bulk path: cp.async.bulk global -> shared -> global through a ring of
 // `stages` shared-memory blocks, driven by one thread; completion of each load
@@ -217,12 +237,15 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 // Acquire-wait on a hop2 tile's flag; the last hop2 tile of the chunk to pass
 // re-arms flag and pass counter so a cached graph replays without a memset.
-__device__ __forceinline__ void wait_tile_flag(const Tile& t, Ctl* ctl) {
+// Returns false on a timeout: the caller skips the tile (staging is never
+// copied unsignalled — the destination keeps its old bytes) and leaves the
+// flag state for mp_sync to re-zero.
+__device__ __forceinline__ bool wait_tile_flag(const Tile& t, Ctl* ctl) {
   const uint64_t t0 = globaltimer();
   while (ld_acquire_sys(t.wait) < t.wait_count) {
-    if (globaltimer() - t0 > kWaitTimeoutNs) {
-      atomicExch(&ctl->error, 1u);
-      break;
+    if (wait_expired(ctl, t0)) {
+      raise_error(ctl, 1u);
+      return false;
     }
     __nanosleep(64);
   }
@@ -230,6 +253,7 @@ __device__ __forceinline__ void wait_tile_flag(const Tile& t, Ctl* ctl) {
     *(volatile uint32_t*)t.pass = 0u;
     *(volatile uint32_t*)t.wait = 0u;
   }
+  return true;
 }
 
 // A tile's completion signal is ONE system-scope release reduction by thread
@@ -263,8 +287,8 @@ __device__ __forceinline__ void group_wait(const GroupSync& g, Ctl* ctl) {
   const uint64_t t0 = globaltimer();
   for (int q = 0; q < g.n; ++q)
     while (ld_acquire_sys(g.gen[q]) < want) {
-      if (globaltimer() - t0 > kWaitTimeoutNs) {
-        atomicExch(&ctl->error, 2u);
+      if (wait_expired(ctl, t0)) {
+        raise_error(ctl, 2u);
         return;
       }
       __nanosleep(128);
@@ -442,7 +466,7 @@ struct TmaEngine {
       const Tile t = pending;
       const int why = blocked;
       blocked = -1;
-      if (t.wait) wait_tile_flag(t, ctl);
+      if (t.wait && !wait_tile_flag(t, ctl)) continue;  // timed out: skip, never copy staging
       if (why == 1 || (((uintptr_t)t.src ^ (uintptr_t)t.dst) & 15u) != 0) {
         *coop = t;
         return 1;
@@ -612,6 +636,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
     // Two barriers per tile.
     __shared__ Tile s_tiles[2];
     __shared__ unsigned s_w[2];
+    __shared__ int s_skip;  // the tile's flag wait timed out: skip it
     const unsigned sig_tid = blockDim.x > 32 ? 32u : 0u;  // a thread of the second warp
     unsigned c1 = ntiles;  // thread 0: claim of the tile after the next one
     if (threadIdx.x == 0) {
@@ -645,7 +670,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
             trace_end(trace, pend_node);
             if (pend_sig) signal_tile(pend_sig, pend_bytes);
           }
-          wait_tile_flag(t, ctl);
+          s_skip = !wait_tile_flag(t, ctl);
         }
         trace_start(trace, t.node);
       }
@@ -654,7 +679,9 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
         trace_end(trace, pend_node);
         if (pend_sig) signal_tile(pend_sig, pend_bytes);
       }
-      if (t.flags & TILE_SRC_MUTABLE)
+      const bool skip = t.wait && s_skip;  // s_skip is only written for waiting tiles
+      if (skip) {
+      } else if (t.flags & TILE_SRC_MUTABLE)
         copy_range<UNROLL, true>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
       else
         copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
@@ -664,7 +691,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       }
       __syncthreads();  // B2: every store of the tile precedes its (deferred) release
       pend = true;
-      pend_sig = t.signal;
+      pend_sig = skip ? nullptr : t.signal;  // a skipped tile never reports bytes
       pend_bytes = sig_bytes(t);
       pend_node = t.node;
       slot ^= 1u;
@@ -697,8 +724,8 @@ __global__ void group_recv_kernel(GroupSync gsync, unsigned long long* done,
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(done) : "memory");
     if (v >= expected) break;
-    if (globaltimer() - t0 > kWaitTimeoutNs) {
-      atomicExch(&ctl->error, 3u);
+    if (wait_expired(ctl, t0)) {
+      raise_error(ctl, 3u);
       break;
     }
     __nanosleep(128);

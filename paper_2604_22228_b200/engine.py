@@ -116,12 +116,20 @@ class Engine:
                   copy: str | None = None, unroll: int | None = None,
                   tma_stages: int | None = None, tma_block: int | None = None,
                   tma_peer: bool | None = None, sched: str | None = None,
-                  small_max_bytes: int | None = None, pdl: int | None = None) -> None:
+                  small_max_bytes: int | None = None, pdl: int | None = None,
+                  wait_timeout_ms: int | None = None, fault_inject: int | None = None) -> None:
         """Pick the copy mechanism per path type and the SM-kernel shape.
         `sched`: "auto" (static one-tile-per-CTA tables when no tile waits or
-        touches host memory) or "dynamic" (atomic tile claims always)."""
+        touches host memory) or "dynamic" (atomic tile claims always).
+        `wait_timeout_ms`: limit of a relay-flag wait (0 = 4 s); a timeout
+        fails every later send until `sync()` reports and clears it.
+        `fault_inject=1` (tests only) mutes one staged chunk's hop1 signal."""
         o = _lib.mp_engine_opts()
         check(lib.mp_ctx_get_engine(self._ctx, C.byref(o)))
+        if wait_timeout_ms is not None:
+            o.wait_timeout_ms = int(wait_timeout_ms)
+        if fault_inject is not None:
+            o.fault_inject = int(fault_inject)
         if small_max_bytes is not None:
             o.small_max_bytes = small_max_bytes
         if pdl is not None:
@@ -324,7 +332,8 @@ class Engine:
         check(lib.mp_wait(self._ctx, handle or None))
 
     def sync(self) -> None:
-        """Wait for every transfer; raises if a relay flag wait timed out."""
+        """Wait for every transfer; raises if a relay flag wait timed out
+        since the last sync (and clears the error, so sends run again)."""
         check(lib.mp_sync(self._ctx))
 
     # -- introspection -------------------------------------------------------

@@ -72,6 +72,26 @@ def test_lru_matches_reference():
         assert [k.src_buffer_id for k in cache.keys()] == case["final_order"]
 
 
+def test_lru_failed_build_leaves_cache_unchanged():
+    """graph.py:173-186: a miss builds before it inserts, so a build that
+    raises leaves the cache as it was and the next access is a plain miss."""
+    topo = mp.load_topology(PLANNER["topologies"][0])
+    cfg = mp.PathConfig()
+    ps = mp.plan_paths(topo, topo.device(0), topo.device(1), cfg)
+    plan = mp.make_chunk_plan(ps, 64, 1)
+    key = mp.graph_key(1, 2, 64, cfg, ps)
+    other = mp.graph_key(3, 4, 64, cfg, ps)
+    cache = mp.GraphCache(2)
+    cache.get_or_build(other, plan)
+    with pytest.raises(Exception):
+        cache.get_or_build(key, None)  # build_graph(None) raises
+    assert len(cache) == 1 and key not in cache
+    assert [k.src_buffer_id for k in cache.keys()] == [3]
+    graph, hit = cache.get_or_build(key, plan)
+    assert hit is False and graph.key == key and len(cache) == 2
+    assert cache.get_or_build(key, plan) == (graph, True)
+
+
 @pytest.mark.parametrize("case", load("topology")["cases"], ids=lambda c: repr(c["text"][:20]))
 def test_topology_parser_matches_reference(case):
     if "error" in case:
