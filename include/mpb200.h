@@ -168,6 +168,9 @@ typedef struct {
 /* Engine knobs (choice of copy mechanism per path type; measured defaults). */
 #define MP_ENGINE_SM 0       /* hand-written sm_100a copy kernel       */
 #define MP_ENGINE_CE 1       /* copy engine cudaMemcpyAsync            */
+#define MP_ENGINE_AUTO 2     /* host path only (default): SM kernels while
+                                every host chunk fits one roundtrip tile
+                                (<= 64 KiB), copy engines above          */
 #define MP_COPY_VEC 0        /* 16-byte vector LDG/STG                 */
 #define MP_COPY_TMA 1        /* cp.async.bulk staged through smem      */
 #define MP_SCHED_AUTO 0      /* static one-tile-per-CTA tables where no
@@ -189,7 +192,8 @@ typedef struct {
   int32_t tma_stages;        /* TMA: shared-memory ring stages (2..16)  */
   int32_t tma_block;         /* TMA: bytes per bulk copy (multiple of 16) */
   int32_t host_engine;       /* MP_ENGINE_*: host-staged path by the SM
-                                kernels (mapped pinned memory) or by CEs */
+                                kernels (mapped pinned memory), by CEs,
+                                or MP_ENGINE_AUTO (default)              */
   int32_t tma_peer;          /* 1: TMA bulk copies also on tables that touch
                                 another GPU over NVLink; 0 (default): such
                                 tables run the 16-byte LDG/STG kernel;

@@ -34,7 +34,7 @@ MP_PATH_DIRECT, MP_PATH_GPU, MP_PATH_HOST = 0, 1, 2
 MP_ROLE_DIRECT, MP_ROLE_HOP1, MP_ROLE_HOP2 = 0, 1, 2
 MP_SHARE_BANDWIDTH, MP_SHARE_EQUAL = 0, 1
 MP_DUPLEX_FULL, MP_DUPLEX_HALF = 0, 1
-MP_ENGINE_SM, MP_ENGINE_CE = 0, 1
+MP_ENGINE_SM, MP_ENGINE_CE, MP_ENGINE_AUTO = 0, 1, 2
 MP_COPY_VEC, MP_COPY_TMA = 0, 1
 MP_SCHED_AUTO, MP_SCHED_DYNAMIC = 0, 1
 

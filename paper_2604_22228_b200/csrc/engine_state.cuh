@@ -14,7 +14,7 @@ namespace {
   } while (0)
 
 using KernelFn = void (*)(const mpk::Tile*, unsigned, mpk::Ctl*, unsigned, unsigned, unsigned,
-                          unsigned long long*, mpk::GroupSync, mpk::Sched*);
+                          unsigned long long*, mpk::GroupSync, mpk::Sched*, unsigned);
 
 KernelFn pick_kernel(const mp_engine_opts& o) {
   if (o.copy_kind == MP_COPY_TMA) return mpk::transfer_kernel<1, 8>;
@@ -84,7 +84,7 @@ void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, 
                      unsigned ntiles, mpk::Ctl* ctl, unsigned nstatic,
                      unsigned long long* trace = nullptr, const mpk::GroupSync* gsync = nullptr,
                      bool peer = false, int sms = 148, const mpk::SmallTable<mpk::kSmallMaxTiles>* small = nullptr,
-                     int kind = PROG_DYNAMIC, mpk::Sched* sched = nullptr) {
+                     int kind = PROG_DYNAMIC, mpk::Sched* sched = nullptr, unsigned nhelp = 0) {
   if (kind == PROG_SMALL && small && !trace && !gsync) {
     // programmatic dependent launch (opts.pdl) from kPdlMinBytes: the kernel
     // waits on griddepcontrol before any memory access, so stream order holds
@@ -141,7 +141,7 @@ void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, 
   lc.attrs = attr;
   lc.numAttrs = (o_in.pdl >= 3 || (o_in.pdl >= 2 && kind != PROG_DYNAMIC)) && !trace && !gsync ? 1 : 0;
   CK(cudaLaunchKernelEx(&lc, fn, tiles, ntiles, ctl, (unsigned)o.tma_stages, (unsigned)o.tma_block,
-                        nstatic, trace, g, sched));
+                        nstatic, trace, g, sched, nhelp));
 }
 
 double now_us() {
@@ -209,6 +209,7 @@ struct Program {
   int kind = PROG_DYNAMIC;                 // ProgKind
   std::shared_ptr<mpk::SmallTable<mpk::kSmallMaxTiles>> small;  // PROG_SMALL: the table as kernel params
   uint64_t bytes = 0;    // PROG_SMALL: bytes the table moves
+  unsigned nhelp = 0;    // PROG_STATIC_TMA: trailing host-path tiles worked by helper warps
 };
 
 // Hash of a cache key (raw bytes: pointers, sizes, devices, config; up to

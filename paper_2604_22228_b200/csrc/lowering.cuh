@@ -8,6 +8,13 @@ namespace {
 
 // Host-path tiles stay small so many CTAs keep PCIe requests in flight.
 constexpr uint64_t kHostTileBytes = 64 << 10;
+// A host-staged chunk up to this size, with source and destination on one
+// device, moves as ONE roundtrip tile (mpk::TILE_ROUNDTRIP: hop1, CTA
+// barrier, hop2 in one CTA) — no flag, no system-scope release, no wait, so
+// the table keeps its static schedule; larger chunks are cut into hop1 /
+// hop2 tiles handed off through the chunk's flag (chunk-level hop ordering
+// of the reference's trace needs the whole chunk's hop1 before any hop2).
+constexpr uint64_t kRoundtripMaxBytes = 64 << 10;
 
 // Rounds between a relay chunk's hop1 and hop2 tiles in one table (loopback,
 // or a relay sharing the source GPU): hop2 of round r queues after round
@@ -54,15 +61,16 @@ uint64_t auto_tile_bytes(const mp_ctx* ctx, uint64_t path_bytes, int sms) {
 }
 
 // Interior tile boundaries of [0, len): every `tile` bytes, moved down to a
-// 16-byte-aligned destination address so only a chunk's first and last tiles
-// carry an unaligned head/tail (chunk offsets are mostly unaligned,
-// pipeline.py:66-77).
+// 128-byte-aligned destination address (a whole L2 line) so only a chunk's
+// first and last tiles carry an unaligned head/tail and every interior tile
+// moves whole lines (chunk offsets are mostly unaligned, pipeline.py:66-77;
+// 16-byte cuts measured +2.6% at 128 MiB over 9 chunks).
 std::vector<uint64_t> tile_cuts(uint64_t dst, uint64_t len, uint64_t tile) {
   std::vector<uint64_t> cuts{0};
   uint64_t o = 0;
   while (len - o > tile) {
     uint64_t next = o + tile;
-    uint64_t adj = next - ((dst + next) & 15u);
+    uint64_t adj = next - ((dst + next) & 127u);
     if (adj > o) next = adj;
     cuts.push_back(next);
     o = next;
@@ -119,6 +127,7 @@ class Lowering {
     plan(cfg);
     schedule();
     tiles_.assign(ctx_->phys.size(), {});
+    helpers_.assign(ctx_->phys.size(), {});
     stage_cursor_.assign(ctx_->logi.size(), 0);
     for (int t = 0; t < (int)xs_.size(); ++t) lower_transfer(t);
     upload();
@@ -157,6 +166,9 @@ class Lowering {
   std::vector<uint64_t> static_tile_;
   std::vector<int> static_kind_;
   std::vector<TileList> tiles_;
+  // host-path tiles of a static TMA table, worked by the helper warps
+  // (transfer_kernel nhelp); folded into the front of the table otherwise
+  std::vector<std::vector<mpk::Tile>> helpers_;
   std::vector<uint64_t> stage_cursor_;  // shared relay arenas
   uint64_t host_cursor_ = 0;            // shared pinned arena
   uint32_t node_ = 0;  // logical node id of a chunk's first hop (graph.py:97-117), global
@@ -220,12 +232,22 @@ class Lowering {
           if (rule.host >= 0) host_engine = rule.host;
           break;
         }
+      // MP_ENGINE_AUTO (the default) for the host path: the SM kernels when
+      // every host chunk is one roundtrip tile (<= kRoundtripMaxBytes: the
+      // hops ride inside the direct stream's launch), copy engines for
+      // larger host chunks (a bandwidth-sized PCIe share: 2-D CE copies
+      // measured ~10% ahead of SM-driven PCIe at 128-256 MiB)
+      uint64_t host_nominal = 0;
+      for (size_t p = 0; p < xs_[t].paths.size(); ++p)
+        if (xs_[t].paths[p].kind == MP_PATH_HOST) host_nominal = info_[t][p].nominal;
+      const bool host_sm = host_engine == MP_ENGINE_SM ||
+                           (host_engine == MP_ENGINE_AUTO && host_nominal <= kRoundtripMaxBytes);
       eng_[t] = Engines{direct_engine == MP_ENGINE_SM && sm_ok, o_.relay_engine == MP_ENGINE_SM && sm_ok,
-                        host_engine == MP_ENGINE_SM && sm_ok, 0};
+                        host_sm && sm_ok, 0};
       for (size_t p = 0; p < paths.size(); ++p) {
         const PathInfo& pi = info_[t][p];
         if (paths[p].kind == MP_PATH_GPU) {
-          stage_need[paths[p].stage] += pi.bytes + 16 * (size_t)pi.count;
+          stage_need[paths[p].stage] += pi.bytes + 128 * (size_t)pi.count;
           if (eng_[t].relay_sm) flag_devs[paths[p].stage] = 1;
         }
         if (paths[p].kind == MP_PATH_HOST) {
@@ -233,7 +255,7 @@ class Lowering {
           eng_[t].host_slots = (o_.host_slots > 0 && !eng_[t].host_sm) ? std::min(o_.host_slots, pi.count)
                                                                        : pi.count;
           host_need += eng_[t].host_slots < pi.count ? (size_t)eng_[t].host_slots * pi.nominal
-                                                     : pi.bytes + 16 * (size_t)pi.count;
+                                                     : pi.bytes + 128 * (size_t)pi.count;
           if (eng_[t].host_sm) flag_devs[xs_[t].dd] = 1;
         }
       }
@@ -284,7 +306,7 @@ class Lowering {
     if (o_.sched != MP_SCHED_AUTO || o_.tile_bytes != 0) return;
     std::vector<uint64_t> sm_bytes(nph, 0);
     std::vector<int> segs(nph, 0);
-    std::vector<char> dyn(nph, 0), relayed(nph, 0);
+    std::vector<char> dyn(nph, 0), relayed(nph, 0), helped(nph, 0);
     std::vector<std::vector<std::pair<uint64_t, uint64_t>>> direct_segs(nph);  // (dst, len)
     for (int t = 0; t < T; ++t) {
       const int sp = phys_of(xs_[t].sd), dp = phys_of(xs_[t].dd);
@@ -301,7 +323,17 @@ class Lowering {
           relayed[sp] = 1;
           dyn[phys_of(P.stage)] = 1;
         } else if (P.kind == MP_PATH_HOST && eng_[t].host_sm) {
-          dyn[sp] = dyn[dp] = 1;
+          // same device: roundtrip tiles (helpers) unless the chunk needs
+          // the flag handoff; two devices: hop1 helpers on the source, the
+          // destination's table waits on flags
+          if (sp != dp) {
+            helped[sp] = 1;
+            dyn[dp] = 1;
+          } else if (c.length <= kRoundtripMaxBytes) {
+            helped[sp] = 1;
+          } else {
+            dyn[sp] = 1;
+          }
         }
       }
     }
@@ -313,7 +345,8 @@ class Lowering {
         // mp_send_many): the small-message kernel still takes them in ONE
         // launch slot if a tile size keeps the table within one tile per
         // SM — the smallest 16-byte multiple that does, counted exactly
-        if (relayed[ph] || (uint64_t)segs[ph] > grid || sm_bytes[ph] > (uint64_t)o_.small_max_bytes)
+        if (relayed[ph] || helped[ph] || (uint64_t)segs[ph] > grid ||
+            sm_bytes[ph] > (uint64_t)o_.small_max_bytes)
           continue;
         uint64_t tb = std::max<uint64_t>((sm_bytes[ph] + grid - 1) / grid, kStaticMinTile);
         for (;; tb += tb / 4) {
@@ -326,10 +359,26 @@ class Lowering {
         static_kind_[ph] = PROG_SMALL;
         continue;
       }
-      const bool small = sm_bytes[ph] <= (uint64_t)o_.small_max_bytes;
+      // host-path helper tiles need the TMA kernel's idle warps
+      const bool small = sm_bytes[ph] <= (uint64_t)o_.small_max_bytes && !helped[ph];
       const bool tma = sm_bytes[ph] <= grid * kStaticMaxPerCta && tma_ok(o_, peer_phys_[ph] != 0);
       if (!small && !tma) continue;
       uint64_t tb = (sm_bytes[ph] + (grid - 2 * segs[ph]) - 1) / (grid - 2 * segs[ph]);
+      if (!relayed[ph]) {
+        // direct segments only: the smallest tile whose exact cut count fits
+        // one tile per SM, so no SM idles (8 segments at 64 MiB: 136 -> 148
+        // tiles; the closed form above reserves two cuts per segment)
+        uint64_t x = std::max<uint64_t>((sm_bytes[ph] + grid - 1) / grid, kStaticMinTile);
+        for (int it = 0; it < 256 && x < tb; ++it, x += std::max<uint64_t>(x / 256, 128)) {
+          x = (x + 15) & ~(uint64_t)15;
+          uint64_t n = 0;
+          for (const auto& sg : direct_segs[ph]) n += ntiles_of(sg.first, sg.second, x);
+          if (n <= grid) {
+            tb = x;
+            break;
+          }
+        }
+      }
       tb = std::max<uint64_t>(tb, kStaticMinTile);
       static_tile_[ph] = (tb + 15) & ~(uint64_t)15;
       static_kind_[ph] = small ? PROG_SMALL : PROG_STATIC_TMA;
@@ -410,9 +459,9 @@ class Lowering {
     Logi& L = ctx_->logi[P.stage];
     const int rp = L.phys;
     const int g = chunk_base_[t] + c;  // flag index, unique across the program
-    // staging offset congruent to the source mod 16 keeps hop1 on the vector paths
+    // staging offset congruent to the source mod 128 keeps hop1 on whole lines
     uint64_t& cur = stage_cursor_[P.stage];
-    cur += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)L.stage + cur)) & 15u;
+    cur += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)L.stage + cur)) & 127u;
     uint8_t* stage = L.stage + cur;
     cur += ch.length;
     if (!eng_[t].relay_sm) {
@@ -425,9 +474,12 @@ class Lowering {
     }
     const uint64_t t1 = tile_for(sp, pi.bytes);
     const uint64_t t2 = tile_for(rp, pi.bytes);  // 64 KiB on the LDG/STG kernel (+4% vs auto)
+    // hop1 and hop2 on one device (loopback): release / acquire at GPU scope
+    const uint32_t scope = sp == rp ? mpk::TILE_SCOPE_GPU : 0u;
     mpk::Tile h1{};
     h1.signal = hop1_signal(L.flags + g);
     h1.node = n_a;
+    h1.flags = scope;
     const uint64_t r2 = 2 * (uint64_t)ch.seq;
     append_tiles(tiles_[sp], order(t, r2), s0 + ch.offset, (uint64_t)(uintptr_t)stage, ch.length, t1, h1);
     mpk::Tile h2{};
@@ -435,15 +487,21 @@ class Lowering {
     h2.pass = L.flags + L.flag_cap + g;
     h2.wait_count = (uint32_t)ntiles_of((uint64_t)(uintptr_t)stage, ch.length, t1);
     h2.pass_count = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, t2);
-    h2.flags = mpk::TILE_SRC_MUTABLE;
+    h2.flags = mpk::TILE_SRC_MUTABLE | scope;
     h2.node = n_b;
     append_tiles(tiles_[rp], order(t, r2 + 1 + 2 * kHop2Delay), (uint64_t)(uintptr_t)stage, d0 + ch.offset,
                  ch.length, t2, h2);
   }
 
-  // Host-staged by the SM kernels: hop1 tiles (src device) store into mapped
-  // pinned memory over PCIe, hop2 tiles (dst device) load it back after the
-  // chunk's flag (in dst memory) counts every hop1 tile.
+  // Host-staged by the SM kernels over mapped pinned memory.  Source and
+  // destination on one device and a chunk <= kRoundtripMaxBytes: ONE
+  // roundtrip tile (hop1, CTA barrier, hop2 in one CTA).  Otherwise hop1
+  // tiles (src device) store into the slot and release the chunk's flag (in
+  // dst memory); hop2 tiles (dst device) load it back once the flag counts
+  // every hop1 tile.  On a static TMA table the host tiles of the source
+  // device go to the helper warps; elsewhere they lead the table (key t),
+  // hop2 tiles right behind their hop1 (a hop2 tile waits only on hop1
+  // tiles claimed before it by resident CTAs).
   void lower_host_sm(int t, int c, const mp_chunk& ch, const PathInfo& pi, uint32_t n_a, uint32_t n_b) {
     const Xfer& x = xs_[t];
     const int sp = phys_of(x.sd), dp = phys_of(x.dd);
@@ -452,26 +510,43 @@ class Lowering {
     Logi& L = ctx_->logi[x.dd];
     uint8_t* host_dev = nullptr;
     CK(cudaHostGetDevicePointer((void**)&host_dev, ctx_->host_stage, 0));
-    host_cursor_ += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)host_dev + host_cursor_)) & 15u;
+    host_cursor_ += ((s0 + ch.offset) - ((uint64_t)(uintptr_t)host_dev + host_cursor_)) & 127u;
     uint8_t* slot = host_dev + host_cursor_;
     host_cursor_ += ch.length;
+    const bool help = static_kind_[sp] == PROG_STATIC_TMA;
+    (void)n_b;
+    if (sp == dp && ch.length <= kRoundtripMaxBytes) {
+      mpk::Tile rt{};
+      rt.src = s0 + ch.offset;
+      rt.dst = d0 + ch.offset;
+      rt.stage = slot;
+      rt.len = ch.length;
+      rt.flags = mpk::TILE_ROUNDTRIP;
+      rt.node = n_a;  // hop2 is n_a + 1 == n_b
+      if (help) helpers_[sp].push_back(rt);
+      else tiles_[sp].push_back({{(uint64_t)t, tiles_[sp].size()}, rt});
+      return;
+    }
+    const uint32_t scope = sp == dp ? mpk::TILE_SCOPE_GPU : 0u;
     const uint64_t th = std::min<uint64_t>(auto_tile_bytes(ctx_, pi.bytes, ctx_->phys[sp].sms), kHostTileBytes);
     mpk::Tile h1{};
     h1.signal = hop1_signal(L.flags + g);
     h1.node = n_a;
-    append_tiles(tiles_[sp], (uint64_t)t, s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
+    h1.flags = scope;
+    TileList h1t;
+    append_tiles(h1t, (uint64_t)t, s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
+    for (auto& kv : h1t) {
+      if (help && sp != dp) helpers_[sp].push_back(kv.second);
+      else tiles_[sp].push_back({{(uint64_t)t, tiles_[sp].size()}, kv.second});
+    }
     mpk::Tile h2{};
     h2.wait = L.flags + g;
     h2.pass = L.flags + L.flag_cap + g;
-    h2.wait_count = (uint32_t)ntiles_of((uint64_t)(uintptr_t)slot, ch.length, th);
+    h2.wait_count = (uint32_t)h1t.size();
     h2.pass_count = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, th);
-    h2.flags = mpk::TILE_SRC_MUTABLE;
+    h2.flags = mpk::TILE_SRC_MUTABLE | scope;
     h2.node = n_b;
-    // every hop2 tile queues after the first two rounds: its hop1 tiles were
-    // front-loaded, so it rarely waits, and no PCIe-latency tile is left for
-    // the tail of the HBM/NVLink stream
-    append_tiles(tiles_[dp], order(t, std::min<uint64_t>(2 * (uint64_t)ch.seq + 3, 3)),
-                 (uint64_t)(uintptr_t)slot, d0 + ch.offset, ch.length, th, h2);
+    append_tiles(tiles_[dp], (uint64_t)t, (uint64_t)(uintptr_t)slot, d0 + ch.offset, ch.length, th, h2);
   }
 
   // Host-staged by copy engines through `host_slots` reused staging slots:
@@ -549,14 +624,20 @@ class Lowering {
     DeviceGuard dg;
     for (size_t ph = 0; ph < tiles_.size(); ++ph) {
       auto& v = tiles_[ph];
-      if (v.empty()) continue;
+      auto& hv = helpers_[ph];
+      if (v.empty() && hv.empty()) continue;
       std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
       std::vector<mpk::Tile> flat;
-      flat.reserve(v.size());
+      flat.reserve(v.size() + hv.size());
       for (auto& kv : v) flat.push_back(kv.second);
       Program pr;
       pr.phys = (int)ph;
       Phys& P = ctx_->phys[ph];
+      // helper tiles ride behind a static TMA table's own tiles; if the
+      // table is not (or no longer) static they lead it as ordinary tiles
+      const bool as_helpers = !hv.empty() && !flat.empty() && static_tile_[ph] &&
+                              static_kind_[ph] == PROG_STATIC_TMA && flat.size() <= (size_t)P.sms;
+      if (!hv.empty() && !as_helpers) flat.insert(flat.begin(), hv.begin(), hv.end());
       bool waits = false, plain = true;
       for (const auto& tl : flat) {
         waits |= tl.wait != nullptr;
@@ -566,9 +647,14 @@ class Lowering {
       pr.kind = static_tile_[ph] && flat.size() <= (size_t)P.sms ? static_kind_[ph] : PROG_DYNAMIC;
       if (pr.kind == PROG_SMALL && (!plain || flat.size() > mpk::kSmallMaxTiles))
         pr.kind = tma_ok(o_, pr.peer) ? PROG_STATIC_TMA : PROG_DYNAMIC;  // e.g. relay hop1 tiles
-      pr.ntiles = (unsigned)flat.size();
+      if (!hv.empty() && !as_helpers) pr.kind = PROG_DYNAMIC;
       pr.grid = (unsigned)std::min<uint64_t>(flat.size(), pr.kind == PROG_DYNAMIC ? grid_of(ph) : P.sms);
       pr.nstatic = waits ? 0u : pr.grid;
+      if (as_helpers) {
+        flat.insert(flat.end(), hv.begin(), hv.end());
+        pr.nhelp = (unsigned)hv.size();
+      }
+      pr.ntiles = (unsigned)flat.size();
       CK(cudaSetDevice(P.ordinal));
       CK(cudaMalloc(&pr.d_tiles, flat.size() * sizeof(mpk::Tile) + sizeof(mpk::Sched)));
       pr.d_sched = reinterpret_cast<mpk::Sched*>(pr.d_tiles + flat.size());

@@ -84,7 +84,7 @@ void enqueue_group(mp_ctx* ctx, Entry* e, cudaStream_t origin) {
   if (!e->progs.empty()) {
     const Program& pr = e->progs[0];
     launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic, nullptr, &g,
-                    pr.peer, P.sms, pr.small.get(), pr.kind, pr.d_sched);
+                    pr.peer, P.sms, pr.small.get(), pr.kind, pr.d_sched, pr.nhelp);
   } else if (e->grole == 3) {
     mpk::group_recv_kernel<<<1, 32, 0, P.kstream>>>(g, ctx->group->done(ctx->group->rank), e->expected,
                                                     P.ctl);
@@ -135,7 +135,7 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr 
     if (timing) ctx->timed_phys = pr.phys;
     if (timing) CK(cudaEventRecord(S.kt0, origin));
     launch_transfer(ctx->opts, pr.grid, origin, pr.d_tiles, pr.ntiles, S.ctl, pr.nstatic, nullptr,
-                    nullptr, pr.peer, S.sms, pr.small.get(), pr.kind, pr.d_sched);
+                    nullptr, pr.peer, S.sms, pr.small.get(), pr.kind, pr.d_sched, pr.nhelp);
     if (timing) CK(cudaEventRecord(S.kt1, origin));
     return;
   }
@@ -172,7 +172,7 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr 
     if (t) ctx->timed_phys = pr.phys;
     if (t) CK(cudaEventRecord(P.kt0, ks));
     launch_transfer(ctx->opts, pr.grid, ks, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic,
-                    tr ? tr->stamps[pr.phys] : nullptr, nullptr, pr.peer, P.sms, pr.small.get(), pr.kind, pr.d_sched);
+                    tr ? tr->stamps[pr.phys] : nullptr, nullptr, pr.peer, P.sms, pr.small.get(), pr.kind, pr.d_sched, pr.nhelp);
     if (t) CK(cudaEventRecord(P.kt1, ks));
   }
   // copy-engine lanes
@@ -514,9 +514,13 @@ int mp_ctx_create(int32_t n_logical, const int32_t* device_map, mp_ctx** out) {
   ctx->opts.host_slots = 0;
   ctx->opts.pull = 0;
   ctx->opts.sm_min_bytes = 0;
-  // copy engines move the host-staged path: SM bulk copies to/from mapped
-  // pinned memory measured ~10x slower (profiles/r01_exp_host.jsonl)
-  ctx->opts.host_engine = MP_ENGINE_CE;
+  // the SM kernels move a small host-staged share (mapped pinned memory): a
+  // host chunk <= 64 KiB is one roundtrip tile worked beside the direct
+  // stream inside the same launch, so direct + host stays ONE kernel (a PDL
+  // replay); the copy-engine variant (2-D copies, fork/join events) costs a
+  // multi-node graph per send: 64 MiB 27.9 vs 21.0 us, 16 MiB 20.8 vs 6.3 us
+  // (profiles/r02_multifree.jsonl).  Larger host chunks go to copy engines.
+  ctx->opts.host_engine = MP_ENGINE_AUTO;
   ctx->opts.unroll = 8;
   ctx->opts.tma_stages = 4;
   ctx->opts.tma_block = 32768;
@@ -649,7 +653,7 @@ int mp_ctx_set_engine(mp_ctx* ctx, const mp_engine_opts* o) {
   if (o->tma_block < 16 || o->tma_block % 16 || (int64_t)o->tma_block * o->tma_stages > 227 * 1024)
     return fail(MP_ERR_VALUE, "tma_block must be a multiple of 16 with stages*block <= 227 KiB");
   if (o->direct_engine < 0 || o->direct_engine > 1 || o->relay_engine < 0 || o->relay_engine > 1 ||
-      o->host_engine < 0 || o->host_engine > 1)
+      o->host_engine < 0 || o->host_engine > 2)
     return fail(MP_ERR_VALUE, "unknown engine");
   if (o->sched != MP_SCHED_AUTO && o->sched != MP_SCHED_DYNAMIC) return fail(MP_ERR_VALUE, "unknown sched");
   if (o->small_max_bytes < 0 || o->small_max_bytes > (int64_t)1 << 31)
@@ -1085,11 +1089,11 @@ int mp_kernel_bench(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int3
   mp_engine_opts o = ctx->opts;
   o.pdl = 0;
   launch_transfer(o, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
-                  nullptr, pr->peer, S.sms, pr->small.get(), pr->kind, pr->d_sched);  // warm
+                  nullptr, pr->peer, S.sms, pr->small.get(), pr->kind, pr->d_sched, pr->nhelp);  // warm
   CK(cudaEventRecord(S.kt0, S.kstream));
   for (int i = 0; i < reps; ++i)
     launch_transfer(o, pr->grid, S.kstream, pr->d_tiles, pr->ntiles, S.ctl, pr->nstatic, nullptr,
-                    nullptr, pr->peer, S.sms, pr->small.get(), pr->kind, pr->d_sched);
+                    nullptr, pr->peer, S.sms, pr->small.get(), pr->kind, pr->d_sched, pr->nhelp);
   CK(cudaEventRecord(S.kt1, S.kstream));
   CK(cudaEventSynchronize(S.kt1));
   float ms = 0.f;

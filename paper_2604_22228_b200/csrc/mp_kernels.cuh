@@ -26,7 +26,10 @@ struct __align__(16) Tile {
   uint64_t len;          // bytes, >= 1
   uint32_t* signal;      // hop1: flag to release-increment after the copy
   uint32_t* wait;        // hop2: flag to acquire-wait on
-  uint32_t* pass;        // hop2: pass counter next to the flag
+  union {
+    uint32_t* pass;      // hop2: pass counter next to the flag
+    uint8_t* stage;      // TILE_ROUNDTRIP: the staging slot (mapped pinned host memory)
+  };
   uint32_t wait_count;   // hop1 tiles of the chunk
   uint32_t pass_count;   // hop2 tiles of the chunk
   uint32_t flags;        // TILE_* bits
@@ -36,6 +39,14 @@ struct __align__(16) Tile {
 enum : uint32_t {
   TILE_SRC_MUTABLE = 1u,  // source written during this launch (staging): no .nc loads
   TILE_SIGNAL_BYTES = 2u, // signal is a u64 byte counter (+len), not a u32 tile count (+1)
+  // A whole host-staged chunk in ONE CTA (source and destination on one
+  // device): hop1 src -> stage, a CTA barrier, hop2 stage -> dst.  The
+  // barrier orders hop2 after hop1 (graph.py:115-117) with no flag and no
+  // system-scope fence; trace nodes `node` (hop1) and `node + 1` (hop2).
+  TILE_ROUNDTRIP = 4u,
+  // signal / wait at GPU scope: producer and consumer tiles run on the same
+  // device (a relay or host chunk in loopback), so no system-scope release
+  TILE_SCOPE_GPU = 8u,
 };
 
 // Cross-process ordering of consecutive group transfers (multi-process mode):
@@ -88,6 +99,16 @@ __device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void red_release_gpu_add(uint32_t* p, uint32_t v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // 16-byte loads: read-only non-coherent path for immutable sources, L2-only
 // (.cg) for staging written during the launch.
 __device__ __forceinline__ int4 ld16_nc(const void* p) {
@@ -116,30 +137,65 @@ __device__ __forceinline__ void st16(void* p, const int4& v) {
 // thread are in flight before the matching stores.
 template <int UNROLL, bool MUTABLE>
 __device__ __forceinline__ void copy_range(const uint8_t* __restrict__ src,
-                                           uint8_t* __restrict__ dst, uint64_t len) {
-  const unsigned tid = threadIdx.x, nt = blockDim.x;
+                                           uint8_t* __restrict__ dst, uint64_t len,
+                                           unsigned tid, unsigned nt) {
   if ((((uintptr_t)src ^ (uintptr_t)dst) & 15u) == 0) {
     uint64_t head = (16u - ((uintptr_t)dst & 15u)) & 15u;
     if (head > len) head = len;
-    if (tid < head) dst[tid] = MUTABLE ? *(volatile const uint8_t*)(src + tid) : src[tid];
     const uint8_t* s = src + head;
     uint8_t* d = dst + head;
     const uint64_t nvec = (len - head) >> 4;
+    const uint64_t done = head + (nvec << 4);
+    const uint64_t tail = len - done;
+    // the peel's byte loads are issued before the vector loop and stored
+    // after it: an unaligned chunk boundary (most reference chunk offsets
+    // are unaligned) never adds a serial memory latency to its tile
+    const bool hv = tid < head, tv = tid < tail;
+    uint8_t hb = 0, tb = 0;
+    if (hv) hb = MUTABLE ? *(volatile const uint8_t*)(src + tid) : src[tid];
+    if (tv) tb = MUTABLE ? *(volatile const uint8_t*)(src + done + tid) : src[done + tid];
     const int4* s4 = reinterpret_cast<const int4*>(s);
     int4* d4 = reinterpret_cast<int4*>(d);
+    // up to 7 leading vectors reach a 128-byte destination line, so every
+    // warp of the main loop writes (and, src == dst mod 16, reads) whole
+    // lines: a misaligned chunk start costs partial-line traffic in one
+    // tile only (loaded first, stored last, like the byte peel)
+    const uint64_t pre = min(nvec, (uint64_t)(((128u - ((uintptr_t)d & 127u)) & 127u) >> 4));
+    const bool pv = tid < pre;
+    int4 pvec;
+    if (pv) pvec = MUTABLE ? ld16_cg(s4 + tid) : ld16_nc(s4 + tid);
+    s4 += pre;
+    d4 += pre;
+    const uint64_t nmain = nvec - pre;
     const uint64_t step = (uint64_t)nt * UNROLL;
     uint64_t i = tid;
-    for (; i + (uint64_t)(UNROLL - 1) * nt < nvec; i += step) {
+    for (; i + (uint64_t)(UNROLL - 1) * nt < nmain; i += step) {
       int4 v[UNROLL];
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) v[u] = MUTABLE ? ld16_cg(s4 + i + u * nt) : ld16_nc(s4 + i + u * nt);
 #pragma unroll
       for (int u = 0; u < UNROLL; ++u) st16(d4 + i + u * nt, v[u]);
     }
-    for (; i < nvec; i += nt) st16(d4 + i, MUTABLE ? ld16_cg(s4 + i) : ld16_nc(s4 + i));
-    const uint64_t done = head + (nvec << 4);
-    const uint64_t tail = len - done;
-    if (tid < tail) dst[done + tid] = MUTABLE ? *(volatile const uint8_t*)(src + done + tid) : src[done + tid];
+    // the remainder (< UNROLL vectors per thread) as ONE round, every load
+    // before any store (loads clamped to the last vector, stores predicated):
+    // a tile that is not a multiple of UNROLL x 16 x threads bytes — every
+    // tile cut from an unaligned chunk — otherwise ended in up to UNROLL-1
+    // serial load -> store round trips on a few threads, and the last tile
+    // of a table set the kernel's end (+1.7 us at 128 MiB over 9 chunks)
+    if (i < nmain) {
+      int4 v[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const uint64_t k = min(i + (uint64_t)u * nt, nmain - 1);
+        v[u] = MUTABLE ? ld16_cg(s4 + k) : ld16_nc(s4 + k);
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u)
+        if (i + (uint64_t)u * nt < nmain) st16(d4 + i + u * nt, v[u]);
+    }
+    if (pv) st16(d4 - pre + tid, pvec);
+    if (hv) dst[tid] = hb;
+    if (tv) dst[done + tid] = tb;
   } else if ((((uintptr_t)src ^ (uintptr_t)dst) & 3u) == 0) {
     uint64_t head = (4u - ((uintptr_t)dst & 3u)) & 3u;
     if (head > len) head = len;
@@ -242,7 +298,8 @@ __device__ __forceinline__ void fence_proxy_async() {
 // flag state for mp_sync to re-zero.
 __device__ __forceinline__ bool wait_tile_flag(const Tile& t, Ctl* ctl) {
   const uint64_t t0 = globaltimer();
-  while (ld_acquire_sys(t.wait) < t.wait_count) {
+  const bool gpu = t.flags & TILE_SCOPE_GPU;
+  while ((gpu ? ld_acquire_gpu(t.wait) : ld_acquire_sys(t.wait)) < t.wait_count) {
     if (wait_expired(ctl, t0)) {
       raise_error(ctl, 1u);
       return false;
@@ -267,17 +324,38 @@ __device__ __forceinline__ void release_signal(uint32_t* sig) {
   red_release_sys_add(sig, 1u);
 }
 
-// Completion signal of a tile: +1 on a u32 flag, or +bytes on a u64 counter.
-__device__ __forceinline__ void signal_tile(uint32_t* sig, uint64_t bytes) {
-  if (!bytes) {
+// Completion signal of a tile, by mode (sig_bytes): 0 = +1 on a u32 flag at
+// system scope, kSigGpu = +1 at GPU scope (TILE_SCOPE_GPU), else +bytes on a
+// u64 byte counter (TILE_SIGNAL_BYTES, group mode).
+constexpr uint64_t kSigGpu = ~0ull;
+__device__ __forceinline__ void signal_tile(uint32_t* sig, uint64_t mode) {
+  if (mode == 0) {
     release_signal(sig);
-    return;
+  } else if (mode == kSigGpu) {
+    red_release_gpu_add(sig, 1u);
+  } else {
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(sig), "l"(mode) : "memory");
   }
-  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(sig), "l"(bytes) : "memory");
 }
 
 __device__ __forceinline__ uint64_t sig_bytes(const Tile& t) {
-  return (t.flags & TILE_SIGNAL_BYTES) ? t.len : 0ull;
+  return (t.flags & TILE_SIGNAL_BYTES) ? t.len : (t.flags & TILE_SCOPE_GPU) ? kSigGpu : 0ull;
+}
+
+// A TILE_ROUNDTRIP tile by threads [tid0, tid0 + nt) of the CTA: hop1 into
+// the staging slot, a barrier over exactly those threads (named barrier
+// `bar`, or the CTA barrier when bar == 0), hop2 out of it with L2 loads.
+template <int UNROLL>
+__device__ __forceinline__ void roundtrip(const Tile& t, unsigned tid, unsigned nt, unsigned bar,
+                                          unsigned long long* trace, bool lead) {
+  copy_range<UNROLL, false>((const uint8_t*)t.src, t.stage, t.len, tid, nt);
+  if (bar) asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nt) : "memory");
+  else __syncthreads();
+  if (lead && trace) {
+    atomicMax(&trace[2 * t.node + 1], (unsigned long long)globaltimer());
+    atomicMin(&trace[2 * (t.node + 1)], (unsigned long long)globaltimer());
+  }
+  copy_range<UNROLL, true>(t.stage, (uint8_t*)t.dst, t.len, tid, nt);
 }
 
 // Group barrier prologue (thread 0 of every CTA) with the 4 s safety timeout.
@@ -344,6 +422,7 @@ struct TmaEngine {
   uint64_t lsig_bytes = 0;
   uint32_t lnode_end = 0;
   int blocked = -1;  // -1 none, 0 table exhausted, 1 misaligned tile, 2 flag wait
+  bool peel_help = false;  // all-static table, CTA >= 64 threads: warps 1.. copy plain tiles' peels
   Tile pending;
   uint64_t g_load = 0, g_store = 0;
 
@@ -357,7 +436,9 @@ struct TmaEngine {
     const uint64_t tail_at = head + body;
     const uint64_t tail = t.len - tail_at;
     trace_start(trace, t.node);
-    if (head | tail) {  // < 16 + 16 bytes: issue every load before any store
+    // a static table's plain tile leaves its peel to warps 1.. (kernel
+    // prologue), so no scalar load latency precedes the bulk stream
+    if ((head | tail) && !(peel_help && !t.signal)) {  // < 16 + 16 bytes: every load before any store
       uint8_t hb[15], tb[15];
 #pragma unroll
       for (int k = 0; k < 15; ++k) {
@@ -414,7 +495,7 @@ struct TmaEngine {
       claim2 = next_claim < ntiles ? claim() : ntiles;
       if (next_claim < ntiles) ahead = tiles[next_claim];
       const bool aligned = (((uintptr_t)t.src ^ (uintptr_t)t.dst) & 15u) == 0;
-      if (t.wait || !aligned) {
+      if (t.wait || !aligned || (t.flags & TILE_ROUNDTRIP)) {  // roundtrips: the whole CTA
         pending = t;
         blocked = t.wait ? 2 : 1;
         return false;
@@ -467,7 +548,7 @@ struct TmaEngine {
       const int why = blocked;
       blocked = -1;
       if (t.wait && !wait_tile_flag(t, ctl)) continue;  // timed out: skip, never copy staging
-      if (why == 1 || (((uintptr_t)t.src ^ (uintptr_t)t.dst) & 15u) != 0) {
+      if (why == 1 || (((uintptr_t)t.src ^ (uintptr_t)t.dst) & 15u) != 0 || (t.flags & TILE_ROUNDTRIP)) {
         *coop = t;
         return 1;
       }
@@ -520,7 +601,7 @@ __device__ __forceinline__ void small_copy_body(uint64_t src_addr, uint64_t dst_
   uint8_t* dst = (uint8_t*)dst_addr;
   const uint32_t tid = threadIdx.x, nt = blockDim.x;
   if ((((uintptr_t)src ^ (uintptr_t)dst) & 15u) != 0) {
-    copy_range<4, false>(src, dst, len);
+    copy_range<4, false>(src, dst, len, threadIdx.x, blockDim.x);
     return;
   }
   uint32_t head = (16u - ((uint32_t)(uintptr_t)dst & 15u)) & 15u;
@@ -565,10 +646,16 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
                                                        unsigned stages, unsigned block,
                                                        unsigned nstatic,
                                                        unsigned long long* trace,
-                                                       GroupSync gsync, Sched* sched) {
+                                                       GroupSync gsync, Sched* sched,
+                                                       unsigned nhelp) {
   // programmatic dependent launch (static tables, engine option pdl): no
   // global access before the previous grid has completed (a no-op otherwise)
   griddep_wait();
+  // Helper tiles (TMA kernel, static tables only): the last `nhelp` tiles are
+  // host-path tiles worked by warps 1.. of CTA (j mod gridDim.x) while thread
+  // 0 streams the CTA's own tile through the TMA ring — PCIe latency overlaps
+  // the HBM/NVLink stream inside one launch, and the table stays static.
+  ntiles -= nhelp;
   // Tiles [0, nstatic) (a prefix with no flag waits, nstatic <= gridDim.x) are
   // taken by CTA blockIdx.x without a claim; the rest are claimed dynamically.
   // A fully static table (nstatic == ntiles: one tile per CTA, no waits) runs
@@ -598,10 +685,51 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
                   trace};
     eng.nstatic = nstatic;
     eng.ctr = ctr;
+    eng.peel_help = all_static && blockDim.x >= 64;
     if (threadIdx.x == 0) {
       for (unsigned s = 0; s < stages; ++s) mbar_init(&s_bar[s], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       eng.prime();
+    }
+    if (threadIdx.x >= 32) {
+      // warps 1..: (a) the unaligned head / tail bytes (< 16 each) of this
+      // CTA's own plain tile, loaded first and stored last, while thread 0
+      // streams its 16-byte-aligned body; (b) the helper tiles of this CTA
+      const unsigned htid = threadIdx.x - 32, hnt = blockDim.x - 32;
+      uint8_t* peel_dst = nullptr;
+      uint8_t peel = 0;
+      if (all_static && blockIdx.x < ntiles) {
+        const Tile t = tiles[blockIdx.x];
+        if (!t.signal && (((uintptr_t)t.src ^ (uintptr_t)t.dst) & 15u) == 0) {
+          uint64_t head = (16u - ((uintptr_t)t.dst & 15u)) & 15u;
+          if (head > t.len) head = t.len;
+          const uint64_t tail_at = head + ((t.len - head) & ~(uint64_t)15);
+          uint64_t o = ~0ull;
+          if (htid < head) o = htid;
+          else if (htid >= 16 && htid - 16 < t.len - tail_at) o = tail_at + htid - 16;
+          if (o != ~0ull) {
+            peel = ((const uint8_t*)t.src)[o];
+            peel_dst = (uint8_t*)t.dst + o;
+          }
+        }
+      }
+      for (unsigned j = blockIdx.x; j < nhelp; j += gridDim.x) {
+        const Tile t = tiles[ntiles + j];
+        if (htid == 0) trace_start(trace, t.node);
+        if (t.flags & TILE_ROUNDTRIP) {
+          roundtrip<UNROLL>(t, htid, hnt, 1, trace, htid == 0);
+          asm volatile("bar.sync 1, %0;" ::"r"(hnt) : "memory");
+          if (htid == 0) trace_end(trace, t.node + 1);
+        } else {  // hop1 to host memory (the destination GPU's kernel runs hop2)
+          copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len, htid, hnt);
+          asm volatile("bar.sync 1, %0;" ::"r"(hnt) : "memory");
+          if (htid == 0) {
+            trace_end(trace, t.node);
+            if (t.signal) signal_tile(t.signal, sig_bytes(t));
+          }
+        }
+      }
+      if (peel_dst) *peel_dst = peel;
     }
     for (;;) {
       if (threadIdx.x == 0) {
@@ -611,13 +739,16 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       __syncthreads();
       if (s_cmd == 0) break;
       const Tile& t = s_tile;
-      if (t.flags & TILE_SRC_MUTABLE)
-        copy_range<UNROLL, true>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
+      const bool rt = t.flags & TILE_ROUNDTRIP;
+      if (rt)
+        roundtrip<UNROLL>(t, threadIdx.x, blockDim.x, 0, trace, threadIdx.x == 0);
+      else if (t.flags & TILE_SRC_MUTABLE)
+        copy_range<UNROLL, true>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len, threadIdx.x, blockDim.x);
       else
-        copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
+        copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len, threadIdx.x, blockDim.x);
       __syncthreads();  // every thread's stores precede the release
       if (threadIdx.x == 0) {
-        trace_end(trace, t.node);
+        trace_end(trace, rt ? t.node + 1 : t.node);
         if (t.signal) signal_tile(t.signal, sig_bytes(t));
       }
     }
@@ -681,10 +812,12 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       }
       const bool skip = t.wait && s_skip;  // s_skip is only written for waiting tiles
       if (skip) {
-      } else if (t.flags & TILE_SRC_MUTABLE)
-        copy_range<UNROLL, true>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
+      } else if (t.flags & TILE_ROUNDTRIP)  // <= 64 KiB, latency-bound: a narrow unroll (no spills)
+        roundtrip<4>(t, threadIdx.x, blockDim.x, 0, trace, threadIdx.x == 0);
+      else if (t.flags & TILE_SRC_MUTABLE)
+        copy_range<UNROLL, true>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len, threadIdx.x, blockDim.x);
       else
-        copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len);
+        copy_range<UNROLL, false>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len, threadIdx.x, blockDim.x);
       if (threadIdx.x == 0) {
         s_tiles[slot ^ 1u] = next;
         s_w[slot ^ 1u] = wn;
@@ -693,7 +826,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       pend = true;
       pend_sig = skip ? nullptr : t.signal;  // a skipped tile never reports bytes
       pend_bytes = sig_bytes(t);
-      pend_node = t.node;
+      pend_node = (t.flags & TILE_ROUNDTRIP) ? t.node + 1 : t.node;
       slot ^= 1u;
     }
     if (threadIdx.x == sig_tid && pend) {

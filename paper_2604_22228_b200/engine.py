@@ -21,12 +21,13 @@ import ctypes as C
 from dataclasses import dataclass
 
 from . import _lib, _mpfast
-from ._lib import MP_COPY_TMA, MP_COPY_VEC, MP_ENGINE_CE, MP_ENGINE_SM, EngineError, check, lib
+from ._lib import (MP_COPY_TMA, MP_COPY_VEC, MP_ENGINE_AUTO, MP_ENGINE_CE, MP_ENGINE_SM, EngineError,
+                   check, lib)
 from .paths import PathConfig, _paths_from_abi
 from .pipeline import ChunkAssignment
 from .topology import Topology, load_topology, mesh_text
 
-ENGINES = {"sm": MP_ENGINE_SM, "ce": MP_ENGINE_CE}
+ENGINES = {"sm": MP_ENGINE_SM, "ce": MP_ENGINE_CE, "auto": MP_ENGINE_AUTO}
 COPIES = {"vec": MP_COPY_VEC, "tma": MP_COPY_TMA}
 KERNELS = {0: "mpk::transfer_kernel<0,8> (16-byte LDG/STG, dynamic tile claims)",
            1: "mpk::transfer_kernel<1,8> (TMA bulk ring)",

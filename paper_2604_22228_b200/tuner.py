@@ -113,7 +113,12 @@ def measure_makespan(engine, config: PathConfig, size: int, src, dst, stream,
 
 def tune(engine, sizes: list[int], grid: list[GridPoint] | None = None,
          modes: tuple[str, ...] = MODES, reps: int = 50, device=None) -> TuningTable:
-    """Time every grid point per (size, mode) on the GPU; record the argmin."""
+    """Time every grid point per (size, mode) on the GPU; record the argmin.
+
+    The reference's `tune(topology, sizes, grid, modes)` (tuner.py:102-124)
+    predicts makespans from a Topology; this one measures, so its first
+    argument is an `Engine` (whose `.topology` is the planning topology) —
+    the only signature difference.  Same grid, tie-break and TuningTable."""
     import torch
     if not sizes:
         raise ValueError("size list is empty")
@@ -137,6 +142,9 @@ def tune(engine, sizes: list[int], grid: list[GridPoint] | None = None,
                 key = (t, p.gpu_paths, p.max_chunks, p.host)
                 if best_key is None or key < best_key:
                     best_key, best = key, TuningEntry(size, mode, p, t)
+            if best is None:
+                raise ValueError(f"no grid point is feasible on {n} accelerators "
+                                 f"(every point needs more than {n - 1} GPU paths)")
             entries.append(best)
     engine.clear_cache()
     return TuningTable(engine.topology.name, entries)
@@ -180,8 +188,8 @@ def tune_engines(engine, sizes: list[int], reps: int = 50, mode: str = GRAPH_MOD
             t = measure_makespan(engine, multi, s, big[:s], out[:s], stream, reps)
             trials.append({"bytes": s, "path": "host", "engine": name, "seconds": t})
     engine.set_size_policy([])
-    engine.configure(direct="sm" if saved["direct_engine"] == 0 else "ce",
-                     host="sm" if saved["host_engine"] == 0 else "ce")
+    names = {0: "sm", 1: "ce", 2: "auto"}
+    engine.configure(direct=names[saved["direct_engine"]], host=names[saved["host_engine"]])
     rules: list[tuple[int, str, str]] = []
     for i, s in enumerate(sizes):
         choice = (direct[s], pick("host", s))

@@ -260,6 +260,7 @@ def test_host_path_2d_groups(size, chunks, graph):
     from paper_2604_22228_b200 import Engine, load_topology, mesh_text
     text = mesh_text("loop", 2, 2.0e12, 1, 2e-6, 1.0e12, 10e-6, "full")
     eng = Engine(load_topology(text), [0, 0])
+    eng.configure(host="ce")
     st = _check(eng, text, size, host=True, chunks=chunks, graph=graph, reps=2, seed=13,
                 src_off=3, dst_off=3)
     assert st.ce_copies <= 2 * 5
