@@ -84,3 +84,57 @@ def test_tma_on_peer_addresses(size):
                         threads=128)
     _check(eng, text, size, min(_ngpu(), 3) - 1 if _ngpu() >= 3 else 1, False, 4, True)
     eng.close()
+
+
+@needs2
+@pytest.mark.parametrize("host", ["sm", "ce", "auto"])
+@pytest.mark.parametrize("host_bw", [1e9, 5.5e10])
+def test_config1_on_real_peers(host, host_bw):
+    """BASELINE config 1 on two GPUs: direct + host at 64 MiB, host hops by
+    the SM kernels (hop1 helpers on GPU0, hop2 flag waits on GPU1), by copy
+    engines, or the per-share automatic choice; tiny and bandwidth-sized
+    host shares."""
+    from paper_2604_22228_b200 import Engine, load_topology, mesh_text
+    text = mesh_text("node", 2, 7.7e11, 1, 2e-6, host_bw, 1e-5, "full")
+    eng = Engine(load_topology(text), [0, 1])
+    eng.configure(host=host)
+    for k in (1, 8):
+        _check(eng, text, 64 * MiB + 13, 1, True, k, True)
+    eng.close()
+
+
+@pytest.mark.skipif(_ngpu() < 4, reason="needs >= 4 GPUs (BASELINE config 3)")
+def test_config3_four_gpus_two_relays_and_host():
+    """BASELINE config 3: direct + relay GPU2 + relay GPU3 + host, 512 MiB."""
+    eng, text = _engine(4)
+    _check(eng, text, 512 * MiB, 3, True, 8, True, reps=1)
+    eng.close()
+
+
+@pytest.mark.skipif(_ngpu() < 8, reason="needs 8 GPUs (BASELINE config 4)")
+@pytest.mark.parametrize("gpu_paths", [1, 2, 4, 7])
+def test_config4_eight_gpus_relay_sweep(gpu_paths):
+    """BASELINE config 4: direct + host + 0..6 relays through GPU2..GPU7, 512 MiB."""
+    eng, text = _engine(8)
+    _check(eng, text, 512 * MiB + 1, gpu_paths, True, 16, True, reps=1)
+    eng.close()
+
+
+@needs2
+def test_ingress_probe_all_peers_to_one_gpu():
+    """The roofline's B_ingress probe (bench.py N > 1): every other GPU
+    writes GPU1 at once as ONE program; the bytes land exactly."""
+    from paper_2604_22228_b200 import PathConfig
+    n = min(_ngpu(), 8)
+    eng, _ = _engine(n)
+    size = 32 * MiB + 3
+    peers = [d for d in range(n) if d != 1]
+    bufs = []
+    for d in peers:
+        s = torch.randint(0, 256, (size,), dtype=torch.uint8, device=f"cuda:{d}")
+        bufs.append((s, torch.zeros(size, dtype=torch.uint8, device="cuda:1"), d))
+    eng.send_many([(s, t, None, d, 1) for s, t, d in bufs], PathConfig(1, False, 1, True))
+    eng.sync()
+    for s, t, _ in bufs:
+        assert torch.equal(s.cpu(), t.cpu())
+    eng.close()
