@@ -73,8 +73,8 @@ int main() {
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  const size_t sizes[] = {4ull << 20, 16ull << 20, 64ull << 20, 128ull << 20};
-  const int hbytes[] = {5 << 10, 64 << 10};
+  const size_t sizes[] = {4096, 64ull << 10, 4ull << 20, 16ull << 20, 64ull << 20, 128ull << 20};
+  const int hbytes[] = {64, 5 << 10, 64 << 10};
   for (size_t bytes : sizes)
     for (int hb : hbytes)
       for (int mode = 0; mode <= 4; ++mode)
