@@ -22,16 +22,20 @@ torch = pytest.importorskip("torch")
 def test_random_transfers_are_byte_exact():
     import paper_2604_22228_b200 as mp
     rng = random.Random(20261017)
-    text = mp.mesh_text("fz", 5, 2.5e12, 1, 2e-6, 40e9, 1e-5, "full")
-    otopo = op.parse_topology(text)
+    # a bandwidth-sized host share (flag-handed-off hop1 / hop2 tiles, CE
+    # groups) and a calibrated-small one (roundtrip tiles, helper warps)
+    texts = {hb: mp.mesh_text("fz", 5, 2.5e12, 1, 2e-6, hb, 1e-5, "full") for hb in (40e9, 1e9)}
+    otopos = {hb: op.parse_topology(t) for hb, t in texts.items()}
     engines = {}
     big_src = torch.empty((100 << 20) + 64, dtype=torch.uint8, device="cuda:0")
     big_dst = torch.empty_like(big_src)
     for it in range(int(os.environ.get("MP_FUZZ_ITERS", 60))):
         knobs = (rng.choice(["tma", "vec"]), rng.choice(["sm", "ce"]), rng.choice(["sm", "ce"]),
-                 rng.choice(["sm", "ce"]), rng.choice(["auto", "dynamic"]), rng.choice([0, -1]))
+                 rng.choice(["sm", "ce", "auto"]), rng.choice(["auto", "dynamic"]), rng.choice([0, -1]),
+                 rng.choice([40e9, 1e9]))
+        otopo = otopos[knobs[6]]
         if knobs not in engines:
-            eng = mp.Engine(mp.load_topology(text), [0] * 5)
+            eng = mp.Engine(mp.load_topology(texts[knobs[6]]), [0] * 5)
             eng.configure(copy=knobs[0], direct=knobs[1], relay=knobs[2], host=knobs[3],
                           sched=knobs[4], tma_peer=knobs[5])
             if knobs[0] == "tma":

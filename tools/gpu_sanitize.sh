@@ -19,8 +19,16 @@ cases = [(dict(copy=copy, host=host), 3, True, 2 * MiB + 7)
          for copy in ("tma", "vec") for host in ("ce", "sm")]
 cases += [({}, 1, False, 4096 + 3), ({}, 1, False, 3 * MiB + 5), ({}, 1, False, 24 * MiB + 9),
           (dict(sched="dynamic"), 1, False, 24 * MiB + 9), (dict(tma_peer=-1), 2, True, 5 * MiB + 1)]
+# round 2: host roundtrip tiles (calibrated-small host share) on the static
+# TMA table's helper warps and on dynamic tables, with and without relays
+small = mp.mesh_text("s1", 4, 2e12, 1, 2e-6, 1e9, 1e-5, "full")
+cases += [(dict(host="sm", _topo=small), 1, True, 24 * MiB + 9),
+          (dict(host="sm", sched="dynamic", _topo=small), 1, True, 24 * MiB + 9),
+          (dict(host="auto", _topo=small), 3, True, 6 * MiB + 3),
+          (dict(host="sm", copy="tma", _topo=small), 2, True, 130 * MiB + 1)]
 for opts, g, host, n in cases:
-    eng = mp.Engine(mp.load_topology(text), [0] * 4)
+    opts = dict(opts)
+    eng = mp.Engine(mp.load_topology(opts.pop("_topo", text)), [0] * 4)
     eng.configure(**opts)
     src = torch.randint(0, 256, (n + 5,), dtype=torch.uint8, device="cuda")[5:]
     dst = torch.zeros(n, dtype=torch.uint8, device="cuda")
