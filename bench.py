@@ -159,7 +159,7 @@ class Clocks:
 def emit(out: dict) -> None:
     """The one result line (kept < 3 KB: optional keys are dropped if needed)."""
     line = json.dumps(out, separators=(",", ":"))
-    for k in ("notes", "multi_over_single", "reference_cpu_path_us", "graph"):
+    for k in ("notes", "errors", "multi_over_single", "reference_cpu_path_us", "graph"):
         if len(line) <= 3000:
             break
         out.pop(k, None)
@@ -383,7 +383,11 @@ def e2e_run(torch, eng, cfg, src, dst, args, sd=0, dd=1, sends_per_input=None, s
     c0.record(cur)
     cs.wait_event(c0)
     run(n)
-    c1.record(out_stream)
+    if out_stream != cur:  # both timing events on the source device
+        fin = torch.cuda.Event()
+        fin.record(out_stream)
+        cur.wait_event(fin)
+    c1.record(cur)
     torch.cuda.synchronize()
     eng.sync()
     assert int(hsum) == want, "e2e checksum differs"
@@ -648,27 +652,52 @@ def run_node(args, rank: int, world: int) -> None:
         t, clocks = headline(torch, eng, cfg, src, dst, args, stream, 0)
         st = eng.stats()
         value = args.steps * W * size / t / 1e9
+        # Everything below the headline is optional evidence: a failure there
+        # is reported in the line ("errors") and never costs the headline.
+        errors = {}
+
+        def opt(name, fn, default=None):
+            try:
+                return fn()
+            except Exception as exc:  # noqa: BLE001 - reported, never fatal
+                errors[name] = str(exc)[:160]
+                try:
+                    torch.cuda.synchronize()
+                    eng.sync()
+                except Exception:  # noqa: BLE001
+                    pass
+                return default
+
         # single-path arms: the SM direct kernel, and cudaMemcpyAsync between
         # the two devices' pointers on a copy engine (the peer-copy baseline)
-        t_sm = time_send(torch, eng, PathConfig(max_chunks=1, graph_mode=True), src, dst, size, 20, stream)
-        ce = Engine(load_topology(text), dmap)
-        ce.configure(direct="ce")
-        t_ce = time_send(torch, ce, PathConfig(max_chunks=1, graph_mode=False), src, dst, size, 20, stream)
-        ce.close()
-        t_stream = time_send(torch, eng, PathConfig(g, host, k, False), src, dst, size, 20, stream)
+        t_sm = opt("single_sm", lambda: time_send(torch, eng, PathConfig(max_chunks=1, graph_mode=True),
+                                                  src, dst, size, 20, stream))
+
+        def ce_arm():
+            ce = Engine(load_topology(text), dmap)
+            ce.configure(direct="ce")
+            try:
+                return time_send(torch, ce, PathConfig(max_chunks=1, graph_mode=False), src, dst, size, 20,
+                                 stream)
+            finally:
+                ce.close()
+        t_ce = opt("peer_memcpy", ce_arm)
+        t_stream = opt("streamed", lambda: time_send(torch, eng, PathConfig(g, host, k, False), src, dst,
+                                                     size, 20, stream))
         # roofline constituents measured on this box: per-path probe (direct
         # GPU0->GPU1 and PCIe) and the destination's NVLink ingress with every
         # other GPU writing to GPU1 at once (one program, direct paths only)
-        probe = eng.measure_paths(0, 1, 256 * MiB, 5)
+        probe = opt("probe", lambda: eng.measure_paths(0, 1, 256 * MiB, 5),
+                    {"direct_sm": float("nan"), "d2h": float("nan"), "h2d": float("nan")})
         pcie = min(probe["d2h"], probe["h2d"])
-        ingress = None
-        if world > 2:
+
+        def ingress_probe():
             peers = [d for d in range(world) if d != 1]
             bufs = [(torch.empty(size // 2, dtype=torch.uint8, device=f"cuda:{dmap[d]}"),
                      torch.empty(size // 2, dtype=torch.uint8, device=f"cuda:{dmap[1]}"), d)
                     for d in peers]
-            xs = [(s_, d_, None, d, 1) for s_, d_, d in bufs]
-            post = eng.prepare_many(xs, PathConfig(1, False, 1, True), stream=stream)
+            post = eng.prepare_many([(s_, d_, None, d, 1) for s_, d_, d in bufs],
+                                    PathConfig(1, False, 1, True), stream=stream)
             for _ in range(3):
                 post()
             torch.cuda.synchronize()
@@ -678,15 +707,21 @@ def run_node(args, rank: int, world: int) -> None:
                 post()
             e1.record(stream)
             torch.cuda.synchronize()
-            ingress = 10 * len(peers) * (size // 2) / (e0.elapsed_time(e1) / 1e3) / 1e9
-            del bufs, xs, post
+            eng.sync()
+            return 10 * len(peers) * (size // 2) / (e0.elapsed_time(e1) / 1e3) / 1e9
+        ingress = opt("ingress", ingress_probe) if world > 2 else None
         nvl = min(probe["direct_sm"] * g, ingress or float("inf"))
         R = nvl + pcie
-        relays = []
-        for gp in range(1, g + 1):
-            tr = time_send(torch, eng, PathConfig(gp, True, k, True), src, dst, size, 10, stream, trials=2)
-            relays.append({"relays": gp - 1, "gbs": round(size / tr / 1e9, 1)})
-        e2e = e2e_run(torch, eng, cfg, src, dst, args, steps=max(2, args.steps // 2))
+
+        def relay_sweep():
+            rows = []
+            for gp in range(1, g + 1):
+                tr = time_send(torch, eng, PathConfig(gp, True, k, True), src, dst, size, 10, stream, trials=2)
+                rows.append({"relays": gp - 1, "gbs": round(size / tr / 1e9, 1)})
+            return rows
+        relays = opt("relay_sweep", relay_sweep, [])
+        e2e = opt("e2e", lambda: e2e_run(torch, eng, cfg, src, dst, args, steps=max(2, args.steps // 2)))
+        gbs = lambda t_: None if t_ is None else size / t_ / 1e9  # noqa: E731
         out = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
@@ -696,12 +731,15 @@ def run_node(args, rank: int, world: int) -> None:
                          "frac": value / R, "traffic": None,
                          "peak_kind": "R = min(paths x probed direct, probed dst ingress) + probed PCIe"},
             "path_roofline": {"R_gbs": R, "direct_probe_gbs": probe["direct_sm"], "ingress_gbs": ingress,
-                              "pcie_probed_gbs": pcie, "single_path_sm_gbs": size / t_sm / 1e9,
-                              "peer_memcpy_ce_gbs": size / t_ce / 1e9,
-                              "multi_streamed_gbs": size / t_stream / 1e9, "relay_sweep": relays},
-            "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": size, "d2h_bytes_per_step": 8},
+                              "pcie_probed_gbs": pcie, "single_path_sm_gbs": gbs(t_sm),
+                              "peer_memcpy_ce_gbs": gbs(t_ce),
+                              "multi_streamed_gbs": gbs(t_stream), "relay_sweep": relays},
+            "e2e": ({"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": size, "d2h_bytes_per_step": 8}
+                    if e2e else {"unavailable": errors.get("e2e", "")}),
             "gpu_launches": args.steps * W * st.kernels, "clocks": clocks,
         }
+        if errors:
+            out["errors"] = errors
         eng.close()
         del src, dst
     # baseline only (never on the path): NCCL send/recv GPU0 -> GPU1 between ranks
