@@ -18,10 +18,13 @@ constexpr uint64_t kRoundtripMaxBytes = 64 << 10;
 
 // Rounds between a relay chunk's hop1 and hop2 tiles in one table (loopback,
 // or a relay sharing the source GPU): hop2 of round r queues after round
-// r + kHop2Delay, so the ~600 tiles in flight rarely include a hop2 tile whose
-// hop1 tiles are still being copied (measured, tools/exp_relay.py: 1 relay
-// 1759 -> 1800 GB/s, 6 relays 1384 -> 1420 GB/s vs a delay of 1).
-constexpr uint64_t kHop2Delay = 3;
+// r + kHop2Delay.  Round 1 (system-scope flags) measured delay 3 ahead of 1;
+// with GPU-scope flags and the batched copy remainder, delay 1 is ahead of
+// 0 / 2 / 3 / 5 by 0.5-1.2% across 1-6 relays (tools/exp_relay2.py: 0.971 /
+// 0.972 / 0.963 of the loopback roofline at 1 / 2 / 3 relays, delay 0
+// 0.81-0.92: hop2 tiles then wait).  Cross-device relays are unaffected
+// (the relay's table holds only hop2 tiles).
+constexpr uint64_t kHop2Delay = 1;
 
 // cudaMemcpy2D pitches stay below the device's maximum pitch (2^31 - 1 class)
 constexpr uint64_t kMaxCopyPitch = 1ull << 30;
