@@ -351,7 +351,10 @@ def e2e_run(torch, eng, cfg, src, dst, args, sd=0, dd=1, sends_per_input=None, s
     hsrc = torch.empty(size, dtype=torch.uint8, pin_memory=True)
     hsum = torch.empty(1, dtype=torch.int64, pin_memory=True)
     hsrc.copy_(src.cpu())
-    want = int(src.sum(dtype=torch.int64))
+    # checksum: wrapping int64 sum of the delivered buffer read as 8-byte
+    # words (0.085 ms at 512 MiB; a uint8 -> int64 reduction costs 1.5 ms)
+    words = (lambda t: t.view(torch.int64)) if size % 8 == 0 else (lambda t: t.to(torch.int64))
+    want = int(words(src).sum())
     cur = torch.cuda.current_stream(src.device)
     cs = torch.cuda.Stream(device=src.device)
     bufs = [src, torch.empty_like(src)]
@@ -375,7 +378,7 @@ def e2e_run(torch, eng, cfg, src, dst, args, sd=0, dd=1, sends_per_input=None, s
             if dst.device != src.device:
                 eng.recv(dst, stream=out_stream)
             with torch.cuda.stream(out_stream):
-                hsum.copy_(dst.sum(dtype=torch.int64).view(1), non_blocking=True)
+                hsum.copy_(words(dst).sum().view(1), non_blocking=True)
 
     run(2)
     torch.cuda.synchronize()

@@ -30,8 +30,9 @@ struct __align__(16) Tile {
     uint32_t* pass;      // hop2: pass counter next to the flag
     uint8_t* stage;      // TILE_ROUNDTRIP: the staging slot (mapped pinned host memory)
   };
-  uint32_t wait_count;   // hop1 tiles of the chunk
-  uint32_t pass_count;   // hop2 tiles of the chunk
+  uint32_t wait_count;   // hop1 tiles of the chunk (TILE_ROUNDTRIP: source bytes hop1 adds
+                         // before the chunk to write whole host lines)
+  uint32_t pass_count;   // hop2 tiles of the chunk (TILE_ROUNDTRIP: bytes added after it)
   uint32_t flags;        // TILE_* bits
   uint32_t node;        // logical graph node (chunk-hop) id, for traces
 };
@@ -343,12 +344,15 @@ __device__ __forceinline__ uint64_t sig_bytes(const Tile& t) {
 }
 
 // A TILE_ROUNDTRIP tile by threads [tid0, tid0 + nt) of the CTA: hop1 into
-// the staging slot, a barrier over exactly those threads (named barrier
+// the staging slot (the source lines around the chunk, so the PCIe writes
+// are whole lines; wait_count / pass_count = bytes before / after it), a barrier over exactly those threads (named barrier
 // `bar`, or the CTA barrier when bar == 0), hop2 out of it with L2 loads.
 template <int UNROLL>
 __device__ __forceinline__ void roundtrip(const Tile& t, unsigned tid, unsigned nt, unsigned bar,
                                           unsigned long long* trace, bool lead) {
-  copy_range<UNROLL, false>((const uint8_t*)t.src, t.stage, t.len, tid, nt);
+  // hop1 widened by wait_count / pass_count bytes (whole host lines)
+  copy_range<UNROLL, false>((const uint8_t*)t.src - t.wait_count, t.stage - t.wait_count,
+                            t.len + t.wait_count + t.pass_count, tid, nt);
   if (bar) asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nt) : "memory");
   else __syncthreads();
   if (lead && trace) {

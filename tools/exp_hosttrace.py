@@ -18,10 +18,12 @@ HOST_BW = float(os.environ.get("HOST_BW", "1e9"))
 topo = load_topology(mesh_text("x", 2, 3.2e12, 1, 2e-6, HOST_BW, 1e-5, "full"))
 eng = Engine(topo, [0, 0])
 eng.configure(host=os.environ.get("HOST", "sm"))
-for size in (4 * MiB, 16 * MiB, 128 * MiB):
+SIZES = [int(x) for x in os.environ.get("SIZES", "").split(",") if x] or [4 * MiB, 16 * MiB, 128 * MiB]
+K = int(os.environ.get("K", "8"))
+for size in SIZES:
     src = torch.randint(0, 256, (size,), dtype=torch.uint8, device="cuda")
     dst = torch.empty_like(src)
-    cfg = PathConfig(1, True, 8, False)
+    cfg = PathConfig(1, True, K, False)
     for _ in range(5):
         plan, tl = eng.trace(src, dst, size, cfg, src_dev=0, dst_dev=1)
     rows = []
@@ -29,7 +31,7 @@ for size in (4 * MiB, 16 * MiB, 128 * MiB):
         rows.append({"node": t.node_id, "role": t.role, "start": round(t.start_time * 1e6, 2),
                      "end": round(t.end_time * 1e6, 2), "len": t.length})
     rec = {"size": size, "host": os.environ.get("HOST", "sm"), "rows": rows}
-    print(json.dumps({"size": size, "direct_end": max(r["end"] for r in rows if r["role"] == "direct"),
+    print(json.dumps({"size": size, "k": K, "host_bw": HOST_BW, "direct": [(r["start"], r["end"]) for r in rows if r["role"] == "direct"],
                       "hop1": [(r["start"], r["end"]) for r in rows if r["role"] == "stage_hop1"],
                       "hop2": [(r["start"], r["end"]) for r in rows if r["role"] == "stage_hop2"]}),
           flush=True)
