@@ -92,6 +92,16 @@ def workload_config(args, world: int) -> dict:
             "l2": "inputs larger than L2 (512 MiB > 126 MB), no flush", "parallelism": f"n{world}"}
 
 
+def host_rate(text: str) -> float:
+    """The host-link bandwidth (B/s) a .topo gives the planner (first [hostlink] row)."""
+    rows = text.split("[hostlink]", 1)[1].splitlines() if "[hostlink]" in text else []
+    for line in rows:
+        f = line.split("#", 1)[0].split()
+        if len(f) >= 2:
+            return float(f[1])
+    return float("nan")
+
+
 def cpu_info() -> dict:
     model = ""
     try:
@@ -523,7 +533,7 @@ def run_one(args) -> None:
                      "kernel": st.kernel.split(" ")[0], "kernel_ms": kms,
                      "alg_bytes_per_launch": k_alg, "peak_kind": peak_kind},
         "path_roofline": {"R_gbs": R, "frac": value / R, "hbm_copy_gbs": hbm_peak / 2,
-                          "pcie_probed_gbs": pcie, "host_bw_planning_gbs": 1.0,
+                          "pcie_probed_gbs": pcie, "host_bw_planning_gbs": host_rate(text) / 1e9,
                           "frac_loopback_hbm": value / (hbm_peak / 2),
                           "direct_bytes": direct_bytes, "host_bytes": host_bytes,
                           "single_path_sm_gbs": size / t_sm / 1e9,
@@ -629,6 +639,18 @@ def full_tables(torch, eng, text, dev, stream, size, pcie, hbm_peak) -> dict:
 # ---------------------------------------------------------------------------
 # our arm, N > 1: rank 0 drives GPUs 0..N-1 from one process
 # ---------------------------------------------------------------------------
+_CPU_GROUP = None
+
+
+def cpu_group():
+    """A gloo group over every rank (host-side barriers and object gathers)."""
+    global _CPU_GROUP
+    if _CPU_GROUP is None:
+        import torch.distributed as dist
+        _CPU_GROUP = dist.new_group(backend="gloo") if dist.get_backend() != "gloo" else dist.group.WORLD
+    return _CPU_GROUP
+
+
 def run_node(args, rank: int, world: int) -> None:
     import torch
     import torch.distributed as dist
@@ -643,19 +665,7 @@ def run_node(args, rank: int, world: int) -> None:
     if rank == 0:
         torch.cuda.set_device(0)
         eng = Engine(load_topology(text), dmap)
-        src = torch.randint(0, 256, (size,), dtype=torch.uint8, device="cuda:0",
-                            generator=torch.Generator(device="cuda:0").manual_seed(20261017))
-        dst = torch.zeros(size, dtype=torch.uint8, device=f"cuda:{dmap[1]}")
-        stream = torch.cuda.Stream(device=0)
-        cfg = PathConfig(g, host, k, True)
-        eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
-        eng.sync()
-        torch.cuda.synchronize()
-        assert torch.equal(src.cpu(), dst.cpu()), "delivered bytes differ"
-        t, clocks = headline(torch, eng, cfg, src, dst, args, stream, 0)
-        st = eng.stats()
-        value = args.steps * W * size / t / 1e9
-        # Everything below the headline is optional evidence: a failure there
+        # Everything but the headline is optional evidence: a failure there
         # is reported in the line ("errors") and never costs the headline.
         errors = {}
 
@@ -670,6 +680,31 @@ def run_node(args, rank: int, world: int) -> None:
                 except Exception:  # noqa: BLE001
                     pass
                 return default
+
+        # split ratios from per-path bandwidth measured on this box (north
+        # star subsystem 2): the direct GPU0 -> GPU1 rate, then the host rate
+        # the planner is given is calibrated by measured direct + host sends
+        # (tuner.calibrate_host_bandwidth); the committed .topo is the fallback
+        def plan_topology():
+            from paper_2604_22228_b200.tuner import calibrate_host_bandwidth
+            m = eng.measure_paths(0, 1, 256 * MiB, 5)
+            link = max(m["direct_sm"], m["direct_ce"]) * 1e9
+            hbw, _, _ = calibrate_host_bandwidth(eng, link, size, k, reps=5, name=f"b200_node{world}_probed")
+            return {"source": "probed + calibrated on this box", "link_gbs": link / 1e9,
+                    "host_planning_gbs": hbw / 1e9, "host_engine": {0: "sm", 1: "ce", 2: "auto"}.get(eng.options()["host_engine"])}
+        planning = opt("plan_topology", plan_topology) or {"source": os.path.relpath(topo_file(world), ROOT)}
+        src = torch.randint(0, 256, (size,), dtype=torch.uint8, device="cuda:0",
+                            generator=torch.Generator(device="cuda:0").manual_seed(20261017))
+        dst = torch.zeros(size, dtype=torch.uint8, device=f"cuda:{dmap[1]}")
+        stream = torch.cuda.Stream(device=0)
+        cfg = PathConfig(g, host, k, True)
+        eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
+        eng.sync()
+        torch.cuda.synchronize()
+        assert torch.equal(src.cpu(), dst.cpu()), "delivered bytes differ"
+        t, clocks = headline(torch, eng, cfg, src, dst, args, stream, 0)
+        st = eng.stats()
+        value = args.steps * W * size / t / 1e9
 
         # single-path arms: the SM direct kernel, and cudaMemcpyAsync between
         # the two devices' pointers on a copy engine (the peer-copy baseline)
@@ -739,7 +774,7 @@ def run_node(args, rank: int, world: int) -> None:
                               "multi_streamed_gbs": gbs(t_stream), "relay_sweep": relays},
             "e2e": ({"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": size, "d2h_bytes_per_step": 8}
                     if e2e else {"unavailable": errors.get("e2e", "")}),
-            "gpu_launches": args.steps * W * st.kernels, "clocks": clocks,
+            "gpu_launches": args.steps * W * st.kernels, "clocks": clocks, "planning": planning,
         }
         if errors:
             out["errors"] = errors
@@ -747,7 +782,11 @@ def run_node(args, rank: int, world: int) -> None:
         del src, dst
     # baseline only (never on the path): NCCL send/recv GPU0 -> GPU1 between ranks
     nccl = None
-    dist.barrier()
+    # CPU-side (gloo) waits while rank 0 drives the GPUs: an NCCL barrier is
+    # a spinning kernel, and kernels of another process's context time-slice
+    # with rank 0's kernels on that GPU (no MPS) — relay / destination GPUs
+    # would be shared with the other ranks' barrier kernels
+    dist.barrier(group=cpu_group())
     if dist.get_backend() == "nccl" and rank in (0, 1):
         torch.cuda.set_device(dmap[rank])
         buf = torch.empty(size, dtype=torch.uint8, device=f"cuda:{dmap[rank]}")
@@ -764,7 +803,7 @@ def run_node(args, rank: int, world: int) -> None:
         torch.cuda.synchronize()
         nccl = reps * size / (n0.elapsed_time(n1) / 1e3) / 1e9
     gathered = [None] * world
-    dist.all_gather_object(gathered, nccl)
+    dist.all_gather_object(gathered, nccl, group=cpu_group())
     if rank == 0:
         if gathered[0] and gathered[1]:
             out["path_roofline"]["nccl_p2p_gbs"] = min(gathered[0], gathered[1])
@@ -788,8 +827,9 @@ def main():
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
         dist.init_process_group(backend)
         try:
+            cpu_group()  # collective: every rank creates it up front
             run_node(args, rank, world)
-            dist.barrier()
+            dist.barrier(group=cpu_group())
         finally:
             dist.destroy_process_group()
     else:
