@@ -50,10 +50,13 @@ def _check(eng, text, size, *, gpu_paths=1, host=False, chunks=1, graph=False,
     for r in range(reps):
         data = ot.pattern(size, seed=None if seed is None else seed + r)
         src.copy_(torch.from_numpy(data))
+        dst_buf.fill_(0x5A)  # guard bytes around dst: never written
         dst.copy_(torch.bitwise_not(src))
         eng.send(src, dst, size, cfg, src_dev=0, dst_dev=1)
         eng.sync()
         torch.cuda.synchronize()
+        assert bool((dst_buf[:dst_off] == 0x5A).all()) and bool((dst_buf[dst_off + size:] == 0x5A).all()), \
+            "bytes outside the destination range were written"
         expect = np.empty_like(data)
         ot.run(data, expect, [p["kind"] for p in opaths], ochunks, threads=4)
         got = dst.cpu().numpy()
