@@ -218,8 +218,11 @@ typedef struct {
                                 every later mp_send / mp_send_many /
                                 mp_wait / mp_group_send fails until
                                 mp_sync reports and clears it            */
-  int32_t fault_inject;      /* testing only: 1 = the first staged chunk's
-                                hop1 tiles never signal (forces a timeout) */
+  int32_t fault_inject;      /* testing only, bits: 1 = the first staged
+                                chunk's hop1 tiles never signal (forces a
+                                timeout); 2 = lower loopback devices as
+                                separate GPUs (system-scope flags, host
+                                chunks as hop1 / hop2 tiles) */
 } mp_engine_opts;
 
 /* ---- errors / version ---------------------------------------------------- */

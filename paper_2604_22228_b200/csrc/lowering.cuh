@@ -178,10 +178,15 @@ class Lowering {
   int lane_next_ = 0;
   bool faulted_ = false;  // opts.fault_inject: one staged chunk's hop1 already muted
 
-  // Testing only (opts.fault_inject = 1): the first staged chunk's hop1
+  // Testing only (opts.fault_inject & 2): lower as if every logical device
+  // had its own GPU — system-scope flags, host chunks as hop1 / hop2 tiles
+  // (no roundtrip tiles) — so the cross-device mechanics run on one GPU.
+  bool same_gpu(int a, int b) const { return a == b && (o_.fault_inject & 2) == 0; }
+
+  // Testing only (opts.fault_inject & 1): the first staged chunk's hop1
   // tiles never signal, so its hop2 wait times out (sticky-error tests).
   uint32_t* hop1_signal(uint32_t* flag) {
-    if (o_.fault_inject != 1 || faulted_) return flag;
+    if ((o_.fault_inject & 1) == 0 || faulted_) return flag;
     faulted_ = true;
     return nullptr;
   }
@@ -478,7 +483,7 @@ class Lowering {
     const uint64_t t1 = tile_for(sp, pi.bytes);
     const uint64_t t2 = tile_for(rp, pi.bytes);  // 64 KiB on the LDG/STG kernel (+4% vs auto)
     // hop1 and hop2 on one device (loopback): release / acquire at GPU scope
-    const uint32_t scope = sp == rp ? mpk::TILE_SCOPE_GPU : 0u;
+    const uint32_t scope = same_gpu(sp, rp) ? mpk::TILE_SCOPE_GPU : 0u;
     mpk::Tile h1{};
     h1.signal = hop1_signal(L.flags + g);
     h1.node = n_a;
@@ -524,7 +529,7 @@ class Lowering {
     host_cursor_ += ch.length;
     const bool help = static_kind_[sp] == PROG_STATIC_TMA;
     (void)n_b;
-    if (sp == dp && ch.length <= kRoundtripMaxBytes) {
+    if (same_gpu(sp, dp) && ch.length <= kRoundtripMaxBytes) {
       mpk::Tile rt{};
       rt.src = s0 + ch.offset;
       rt.dst = d0 + ch.offset;
@@ -543,7 +548,7 @@ class Lowering {
       else tiles_[sp].push_back({{(uint64_t)t, tiles_[sp].size()}, rt});
       return;
     }
-    const uint32_t scope = sp == dp ? mpk::TILE_SCOPE_GPU : 0u;
+    const uint32_t scope = same_gpu(sp, dp) ? mpk::TILE_SCOPE_GPU : 0u;
     const uint64_t th = std::min<uint64_t>(auto_tile_bytes(ctx_, pi.bytes, ctx_->phys[sp].sms), kHostTileBytes);
     mpk::Tile h1{};
     h1.signal = hop1_signal(L.flags + g);

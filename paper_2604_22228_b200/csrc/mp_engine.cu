@@ -660,7 +660,7 @@ int mp_ctx_set_engine(mp_ctx* ctx, const mp_engine_opts* o) {
     return fail(MP_ERR_VALUE, "small_max_bytes must be in [0, 2^31]");
   if (o->pdl < 0 || o->pdl > 3) return fail(MP_ERR_VALUE, "pdl must be 0..3");
   if (o->wait_timeout_ms < 0) return fail(MP_ERR_VALUE, "wait_timeout_ms must be >= 0");
-  if (o->fault_inject < 0 || o->fault_inject > 1) return fail(MP_ERR_VALUE, "fault_inject must be 0 or 1");
+  if (o->fault_inject < 0 || o->fault_inject > 3) return fail(MP_ERR_VALUE, "fault_inject must be 0..3");
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
   clear_cache(ctx);

@@ -124,7 +124,9 @@ class Engine:
         touches host memory) or "dynamic" (atomic tile claims always).
         `wait_timeout_ms`: limit of a relay-flag wait (0 = 4 s); a timeout
         fails every later send until `sync()` reports and clears it.
-        `fault_inject=1` (tests only) mutes one staged chunk's hop1 signal."""
+        `fault_inject` (tests only, bits): 1 mutes one staged chunk's hop1
+        signal; 2 lowers logical devices that share a GPU as if they had
+        their own (system-scope flags, host chunks as hop1 / hop2 tiles)."""
         o = _lib.mp_engine_opts()
         check(lib.mp_ctx_get_engine(self._ctx, C.byref(o)))
         if wait_timeout_ms is not None:

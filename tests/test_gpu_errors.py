@@ -85,5 +85,5 @@ def test_wait_options_are_validated():
     with pytest.raises(ValueError):
         eng.configure(wait_timeout_ms=-1)
     with pytest.raises(ValueError):
-        eng.configure(fault_inject=2)
+        eng.configure(fault_inject=4)
     eng.close()

@@ -89,3 +89,17 @@ def test_roundtrip_keeps_hop_order_in_the_trace():
         assert v["stage_hop2"].start_time >= v["stage_hop1"].end_time
         assert v["stage_hop2"].end_time >= v["stage_hop2"].start_time
     eng.close()
+
+
+@pytest.mark.parametrize("gpu_paths,host_bw,size,k", [(1, 1e9, 4 * MiB + 3, 8), (1, 60e9, 64 * MiB + 5, 8),
+                                                      (3, 1e9, 24 * MiB + 17, 8), (4, 60e9, 100 * MiB + 1, 16)])
+@pytest.mark.parametrize("graph", [False, True])
+def test_cross_device_mechanics_in_loopback(gpu_paths, host_bw, size, k, graph):
+    """fault_inject & 2: the lowering treats the logical devices as separate
+    GPUs — relay and host flags released / acquired at system scope, host
+    chunks as hop1 / hop2 tiles handed off through a flag in the
+    destination's memory (never roundtrip tiles) — byte-exact on one GPU."""
+    eng, text = _engine(gpu_paths + 1, host_bw, fault_inject=2)
+    st = _check(eng, text, size, gpu_paths=gpu_paths, host=True, chunks=k, graph=graph, reps=2, seed=k)
+    assert st.ce_copies == 0
+    eng.close()
