@@ -421,24 +421,29 @@ def short_sweep(torch, eng, PathConfig, big, obig, stream, sizes, g, host, k, sd
     return rows
 
 
-def lifecycle(torch, eng, PathConfig, dev, stream, n=2000):
-    """BASELINE config 5 (short form): capture+instantiate per call, cached
-    replay and per-call stream launch of a direct + host send; host µs per
-    message (enqueue only, synced in batches) and GPU latency."""
+def lifecycle(torch, eng, PathConfig, dev, stream, n=10000):
+    """BASELINE config 5: 4 KiB-4 MiB, 10k iterations per arm: capture +
+    instantiate per call, cached replay and per-call stream launch of a
+    direct + host send; host µs per message (enqueue only, synced in
+    batches) and GPU latency."""
     res = []
     big = torch.empty(4 * MiB, dtype=torch.uint8, device=f"cuda:{dev}")
     out = torch.empty_like(big)
-    for size in (4 << 10, 64 << 10, MiB, 4 * MiB):
+    for size in (4 << 10, 16 << 10, 64 << 10, 256 << 10, MiB, 4 * MiB):
         src, dst = big[:size], out[:size]
         g = PathConfig(1, True, 1, True)
         s = PathConfig(1, True, 1, False)
-        cap = []
-        for _ in range(10):
+        cap, phases = [], {p: [] for p in ("creation", "construction", "instantiation", "launch")}
+        for _ in range(20):
             eng.clear_cache()
             eng.send(src, dst, size, g, stream=stream, src_dev=0, dst_dev=1)
             st = eng.stats()
             cap.append(st.creation_us + st.construction_us + st.instantiation_us)
-        row = {"bytes": size, "capture_instantiate_us": statistics.median(cap)}
+            for p in phases:
+                phases[p].append(getattr(st, f"{p}_us"))
+        stream.synchronize()
+        row = {"bytes": size, "capture_instantiate_us": statistics.median(cap),
+               **{f"{p}_us": statistics.median(v) for p, v in phases.items()}}
         for name, cfg in (("replay", g), ("stream", s)):
             for _ in range(10):
                 eng.send(src, dst, size, cfg, stream=stream, src_dev=0, dst_dev=1)
@@ -608,6 +613,19 @@ def full_tables(torch, eng, text, dev, stream, size, pcie, hbm_peak) -> dict:
                              ("tuned", auto, table.config_for(s))):
             row[name] = s / time_send(torch, e, cfg, big[:s], out[:s], s, reps, stream) / 1e9
         rows.append(row)
+    # each figure as a fraction of the roofline: R (bandwidth: HBM copy +
+    # PCIe, loopback) and R_s = S / (t0 + S / R), t0 = the measured one-message
+    # floor (the fastest 1 KiB send of the sweep: launch + completion); from
+    # 16-32 MiB a message is L2-resident in loopback, so R_s can be exceeded
+    R = hbm_peak / 2 + pcie
+    t0 = max(rows[0][k] for k in ("ce_single", "sm_single", "multi_graph", "multi_stream", "tuned"))
+    t0 = rows[0]["bytes"] / (t0 * 1e9)
+    for row in rows:
+        s = row["bytes"]
+        rs = s / (t0 + s / (R * 1e9)) / 1e9
+        row["R_gbs"], row["R_s_gbs"] = R, rs
+        row["multi_frac_R"], row["multi_frac_R_s"] = row["multi_graph"] / R, row["multi_graph"] / rs
+        row["best_frac_R_s"] = max(row[k] for k in ("sm_single", "multi_graph", "tuned")) / rs
     ce.close()
     auto.close()
     del big, out
