@@ -66,6 +66,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
                "-Xcompiler", "-ffp-contract=off", "-I", INCLUDE, "-c", eng_src, "-o", eng_obj]
         if verbose_ptxas:
             cmd[1:1] = ["-Xptxas", "-v"]
+        cmd[1:1] = os.environ.get("MP_NVCC_EXTRA", "").split()  # experiments only
         _run(cmd)
     if force or _stale(LIB, [core_obj, eng_obj]):
         _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", LIB, core_obj, eng_obj,

@@ -347,9 +347,18 @@ __device__ __forceinline__ uint64_t sig_bytes(const Tile& t) {
 // the staging slot (the source lines around the chunk, so the PCIe writes
 // are whole lines; wait_count / pass_count = bytes before / after it), a barrier over exactly those threads (named barrier
 // `bar`, or the CTA barrier when bar == 0), hop2 out of it with L2 loads.
+// `fence`: a system-scope fence after hop2.  hop2 has read back every line
+// hop1 wrote (a PCIe read does not pass an earlier posted write), so the
+// fence is cheap here — and it retires the CTA's host writes early instead
+// of leaving them to the grid-completion flush, which queues behind any
+// saturating H2D DMA (an e2e window's 512 MiB upload: +20 us per 512 MiB
+// message, sends 11.5 -> 10.3 ms per window).  Dynamic tables (large
+// messages, roundtrips far off the critical path) fence; the static TMA
+// table's helper warps do not (at 4-16 MiB the roundtrip is the message's
+// tail and the fence measured +0.8-1.1 us).
 template <int UNROLL>
 __device__ __forceinline__ void roundtrip(const Tile& t, unsigned tid, unsigned nt, unsigned bar,
-                                          unsigned long long* trace, bool lead) {
+                                          unsigned long long* trace, bool lead, bool fence) {
   // hop1 widened by wait_count / pass_count bytes (whole host lines)
   copy_range<UNROLL, false>((const uint8_t*)t.src - t.wait_count, t.stage - t.wait_count,
                             t.len + t.wait_count + t.pass_count, tid, nt);
@@ -360,6 +369,7 @@ __device__ __forceinline__ void roundtrip(const Tile& t, unsigned tid, unsigned 
     atomicMin(&trace[2 * (t.node + 1)], (unsigned long long)globaltimer());
   }
   copy_range<UNROLL, true>(t.stage, (uint8_t*)t.dst, t.len, tid, nt);
+  if (fence) __threadfence_system();
 }
 
 // Group barrier prologue (thread 0 of every CTA) with the 4 s safety timeout.
@@ -721,7 +731,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
         const Tile t = tiles[ntiles + j];
         if (htid == 0) trace_start(trace, t.node);
         if (t.flags & TILE_ROUNDTRIP) {
-          roundtrip<UNROLL>(t, htid, hnt, 1, trace, htid == 0);
+          roundtrip<UNROLL>(t, htid, hnt, 1, trace, htid == 0, false);
           asm volatile("bar.sync 1, %0;" ::"r"(hnt) : "memory");
           if (htid == 0) trace_end(trace, t.node + 1);
         } else {  // hop1 to host memory (the destination GPU's kernel runs hop2)
@@ -745,7 +755,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       const Tile& t = s_tile;
       const bool rt = t.flags & TILE_ROUNDTRIP;
       if (rt)
-        roundtrip<UNROLL>(t, threadIdx.x, blockDim.x, 0, trace, threadIdx.x == 0);
+        roundtrip<UNROLL>(t, threadIdx.x, blockDim.x, 0, trace, threadIdx.x == 0, true);
       else if (t.flags & TILE_SRC_MUTABLE)
         copy_range<UNROLL, true>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len, threadIdx.x, blockDim.x);
       else
@@ -817,7 +827,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
       const bool skip = t.wait && s_skip;  // s_skip is only written for waiting tiles
       if (skip) {
       } else if (t.flags & TILE_ROUNDTRIP)  // <= 64 KiB, latency-bound: a narrow unroll (no spills)
-        roundtrip<4>(t, threadIdx.x, blockDim.x, 0, trace, threadIdx.x == 0);
+        roundtrip<4>(t, threadIdx.x, blockDim.x, 0, trace, threadIdx.x == 0, true);
       else if (t.flags & TILE_SRC_MUTABLE)
         copy_range<UNROLL, true>((const uint8_t*)t.src, (uint8_t*)t.dst, t.len, threadIdx.x, blockDim.x);
       else

@@ -90,15 +90,10 @@ def run(name, eng, cfg, pieces=1, nstreams=1, sends=W):
     print(json.dumps(res), flush=True)
 
 
-cfg = PathConfig(1, True, 8, True)
-eng = Engine(load_topology(text), [0, 0])
-for pieces, ns in ((1, 1), (8, 1), (2, 2), (8, 2), (8, 4), (32, 4)):
-    run("default", eng, cfg, pieces, ns)
-for cps in (1, 2, 3):
-    eng.configure(ctas_per_sm=cps)
-    run(f"ctas_per_sm={cps}", eng, cfg, 8, 2)
-eng.close()
-eng = Engine(load_topology(text), [0, 0])
-eng.configure(direct="ce")
-run("direct=ce", eng, PathConfig(1, False, 1, True), 8, 2)
-eng.close()
+from paper_2604_22228_b200 import mesh_text  # noqa: E402
+HBWS = [float(x) for x in os.environ.get("HBWS", "0.1e9,0.5e9,1e9,2e9").split(",")]
+for hbw in HBWS:
+    eng = Engine(load_topology(mesh_text("x", 2, 3.17e12, 1, 2e-6, hbw, 1e-5, "full")), [0, 0])
+    run(f"direct+host k8 host_bw={hbw:g}", eng, PathConfig(1, True, 8, True), 1, 1)
+    run(f"direct+host k1 host_bw={hbw:g}", eng, PathConfig(1, True, 1, True), 1, 1)
+    eng.close()
