@@ -46,11 +46,11 @@ def rate(eng, cfg, size, reps=300, trials=5):
 
 
 for size in SIZES:
-    for hbw in (0.1e9, 1e9, 4e9):
+    for hbw in [float(x) for x in os.environ.get("HBWS", "0.1e9,1e9,4e9").split(",")]:
         topo = load_topology(mesh_text("x", 2, 3.2e12, 1, 2e-6, hbw, 1e-5, "full"))
         arms = {}
         e = Engine(topo, [0, 0])
-        if hbw == 1e9:
+        if hbw == 1e9 and not os.environ.get("HOST_ONLY"):
             arms["single"] = rate(e, PathConfig(max_chunks=1, graph_mode=True), size)
             arms["direct_k8"] = rate(e, PathConfig(1, False, 8, True), size)
             e.configure(small_max_bytes=0)
@@ -58,9 +58,10 @@ for size in SIZES:
             e.configure(small_max_bytes=4 * MiB)
         e.configure(host="sm")
         arms["host_sm_k8"] = rate(e, PathConfig(1, True, 8, True), size)
-        arms["host_sm_k1"] = rate(e, PathConfig(1, True, 1, True), size)
-        e.configure(pdl=0)
-        arms["host_sm_k8_nopdl"] = rate(e, PathConfig(1, True, 8, True), size)
+        if not os.environ.get("HOST_ONLY"):
+            arms["host_sm_k1"] = rate(e, PathConfig(1, True, 1, True), size)
+            e.configure(pdl=0)
+            arms["host_sm_k8_nopdl"] = rate(e, PathConfig(1, True, 8, True), size)
         e.close()
         for k, v in arms.items():
             print(json.dumps({"size": size, "host_bw": hbw, "arm": k, **v}), flush=True)
