@@ -3,7 +3,8 @@
 Defaults: the bench's headline (512 MiB, direct + host, k=8, graph replay).
 Env: PROF_BYTES, PROF_K, PROF_HOST (1/0), PROF_HOST_BW, PROF_HOST_ENGINE (sm/ce/auto),
 PROF_ITERS, PROF_DEVICES ("0,1": logical GPU0/GPU1 on two physical GPUs; default loopback),
-PROF_GPU_PATHS (1 = direct only; > 1 adds relays through the next logical GPUs)."""
+PROF_GPU_PATHS (1 = direct only; > 1 adds relays through the next logical GPUs),
+PROF_TOPO (a .topo file to plan on instead of the generated mesh, e.g. the bench's)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -14,8 +15,9 @@ dmap = [int(x) for x in os.environ.get("PROF_DEVICES", "0,0").split(",")]
 gp = int(os.environ.get("PROF_GPU_PATHS", 1))
 n = max(len(dmap), gp + 1)
 dmap = (dmap * n)[:n] if len(dmap) < n else dmap
-eng = Engine(load_topology(mesh_text("prof", n, 3.2e12 if len(set(dmap)) == 1 else 7.7e11, 1, 2e-6,
-                                     host_bw, 1e-5, "full")), dmap)
+topo = (open(os.environ["PROF_TOPO"]).read() if os.environ.get("PROF_TOPO") else
+        mesh_text("prof", n, 3.2e12 if len(set(dmap)) == 1 else 7.7e11, 1, 2e-6, host_bw, 1e-5, "full"))
+eng = Engine(load_topology(topo), dmap)
 if os.environ.get("PROF_HOST_ENGINE"):
     eng.configure(host=os.environ["PROF_HOST_ENGINE"])
 src = torch.randint(0, 256, (S,), dtype=torch.uint8, device="cuda")
