@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define MP_ABI_VERSION 3
+#define MP_ABI_VERSION 4
 
 /* ---- status codes -------------------------------------------------------- */
 #define MP_OK 0
@@ -421,10 +421,18 @@ int mp_ipc_close(void* dev_ptr, int32_t device);
  * each relay rank runs its hop2 tiles, the destination rank waits until all
  * bytes landed.  A device-side generation barrier orders consecutive
  * transfers, so cached CUDA graphs replay without host synchronisation.
- * The host-staged path is single-process only. */
+ * The host-staged path needs every rank's host inbox (mp_group_host_arena):
+ * the sender's kernel writes a host chunk into the destination rank's inbox
+ * (shared pinned memory) and releases the chunk's flag in the destination's
+ * HBM; the destination's kernel loads it back. */
 #define MP_GROUP_BLOB_BYTES 256
 int mp_group_create(int32_t nranks, int32_t rank, int32_t device, uint64_t stage_bytes,
                     int32_t flag_cap, mp_ctx** out);
+/* This rank's host inbox for the host-staged path (paths.py:165-166): `bytes`
+ * of POSIX shared memory, pinned and mapped (cudaHostRegister) here and in
+ * every peer at mp_group_import.  Call before mp_group_export; optional
+ * (without it a host-staged plan fails with MP_ERR_STATE). */
+int mp_group_host_arena(mp_ctx* ctx, uint64_t bytes);
 int mp_group_export(const mp_ctx* ctx, uint8_t* blob);
 int mp_group_import(mp_ctx* ctx, int32_t rank, const uint8_t* blob);
 /* Map a peer buffer (handle from mp_ipc_export) into this process, cached. */

@@ -187,6 +187,7 @@ SIGNATURES = {
     "mp_ipc_close": (C.c_int, [_vp, _i32]),
     "mp_group_create": (C.c_int, [_i32, _i32, _i32, _u64, _i32, P(_vp)]),
     "mp_group_export": (C.c_int, [_vp, P(C.c_uint8)]),
+    "mp_group_host_arena": (C.c_int, [_vp, _u64]),
     "mp_group_import": (C.c_int, [_vp, _i32, P(C.c_uint8)]),
     "mp_group_open": (C.c_int, [_vp, P(C.c_uint8), _u64, P(_vp)]),
     "mp_group_send": (C.c_int, [_vp, _vp, C.c_uint32, _vp, _u64, _i32, _i32, P(mp_config), _vp]),

@@ -264,6 +264,13 @@ struct GroupState {
   std::vector<uint32_t*> peer_flags;
   std::vector<size_t> peer_stage_cap;
   std::map<std::string, void*> opened;  // IPC-opened peer buffers by handle
+  // host inboxes (host-staged path): POSIX shm, pinned + mapped in every rank
+  uint8_t* host = nullptr;       // this rank's inbox (host address)
+  uint8_t* host_dev = nullptr;   // ... as the device addresses it
+  size_t host_cap = 0;
+  std::string host_name;         // shm name (unlinked by the owner at destroy)
+  std::vector<uint8_t*> peer_host, peer_host_dev;
+  std::vector<size_t> peer_host_cap;
   uint32_t* gen(int q) { return (uint32_t*)(q == rank ? sync : peer_sync[q]); }
   unsigned long long* done(int q) { return (unsigned long long*)((q == rank ? sync : peer_sync[q]) + 8); }
 };

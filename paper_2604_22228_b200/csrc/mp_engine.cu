@@ -25,8 +25,13 @@
 // engine ops), this file (enqueue / capture / cache lookup, group mode,
 // traces, probes, and the C ABI).
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cerrno>
 #include <chrono>
 #include <functional>
 #include <cstring>
@@ -83,8 +88,17 @@ void enqueue_group(mp_ctx* ctx, Entry* e, cudaStream_t origin) {
   mpk::GroupSync g = group_sync(ctx);
   if (!e->progs.empty()) {
     const Program& pr = e->progs[0];
-    launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic, nullptr, &g,
-                    pr.peer, P.sms, pr.small.get(), pr.kind, pr.d_sched, pr.nhelp);
+    // the receiver's own tiles (host-path hop2) run first, outside the
+    // barrier protocol; its byte-count wait below closes the transfer
+    const bool recv = e->grole == 3;
+    const mpk::GroupSync none{};  // n = 0: no barrier (non-null: no PDL either)
+    launch_transfer(ctx->opts, pr.grid, P.kstream, pr.d_tiles, pr.ntiles, P.ctl, pr.nstatic, nullptr,
+                    recv ? &none : &g, pr.peer, P.sms, pr.small.get(), pr.kind, pr.d_sched, pr.nhelp);
+    if (recv) {
+      mpk::group_recv_kernel<<<1, 32, 0, P.kstream>>>(g, ctx->group->done(ctx->group->rank), e->expected,
+                                                      P.ctl);
+      CK(cudaGetLastError());
+    }
   } else if (e->grole == 3) {
     mpk::group_recv_kernel<<<1, 32, 0, P.kstream>>>(g, ctx->group->done(ctx->group->rank), e->expected,
                                                     P.ctl);
@@ -312,6 +326,8 @@ struct GroupBlob {
   int32_t flag_cap;
   int32_t rank;
   cudaIpcMemHandle_t stage, flags, sync;
+  uint64_t host_cap;   // 0: no host inbox
+  char host_name[40];  // POSIX shm name of the inbox
 };
 static_assert(sizeof(GroupBlob) <= MP_GROUP_BLOB_BYTES, "group blob size");
 
@@ -324,9 +340,9 @@ Entry* build_group_entry(mp_ctx* ctx, const std::string& key, const void* src, u
   e->key = key;
   e->paths = plan_paths(ctx->topo, sr, dr, cfg);
   for (const mp_path& p : e->paths)
-    if (p.kind == MP_PATH_HOST)
-      throw Error{MP_ERR_STATE, "the host-staged path needs a single-process context "
-                                "(group mode moves the NVLink paths)"};
+    if (p.kind == MP_PATH_HOST && ((dr == G->rank && !G->host) || (dr != G->rank && !G->peer_host[dr])))
+      throw Error{MP_ERR_STATE, "the host-staged path needs the destination rank's host inbox "
+                                "(mp_group_host_arena before mp_group_export)"};
   e->chunks = make_chunk_plan(e->paths.data(), (int)e->paths.size(), (int64_t)size, cfg.max_chunks);
   const int np = (int)e->paths.size(), nc = (int)e->chunks.size();
   for (const mp_chunk& c : e->chunks) e->nodes_logical += e->paths[c.path_index].nhops;
@@ -359,6 +375,38 @@ Entry* build_group_entry(mp_ctx* ctx, const std::string& key, const void* src, u
       t.flags = mpk::TILE_SIGNAL_BYTES;
       append_tiles(tiles, 2 * round, s0 + ch.offset, d0 + ch.offset, ch.length,
                    auto_tile_bytes(ctx, path_bytes[p], sms), t);
+      continue;
+    }
+    if (P.kind == MP_PATH_HOST) {
+      // the destination rank's host inbox: the sender's hop1 tiles write the
+      // chunk there and release its flag in the destination's HBM (system
+      // scope), the destination's hop2 tiles load it back once the flag
+      // counts every hop1 tile; offsets / cuts agree across ranks by
+      // construction (congruent to the source mod 16, fixed tile size)
+      stage_off[p] += (((uint64_t)src_align + ch.offset) - stage_off[p]) & 15u;
+      const uint64_t so = stage_off[p];
+      stage_off[p] += ch.length;
+      const size_t cap = dr == me ? G->host_cap : G->peer_host_cap[dr];
+      if (stage_off[p] > cap) throw Error{MP_ERR_STATE, "group host inbox too small for the host share"};
+      const uint64_t th = kGroupRelayTileBytes;
+      if (e->grole == 1) {
+        uint8_t* slot = G->peer_host_dev[dr] + so;
+        mpk::Tile h1{};
+        h1.node = n_a;
+        h1.signal = G->peer_flags[dr] + c;
+        append_tiles(tiles, 2 * round, s0 + ch.offset, (uint64_t)(uintptr_t)slot, ch.length, th, h1);
+      } else if (me == dr) {
+        uint8_t* slot = G->host_dev + so;
+        mpk::Tile h2{};
+        h2.node = n_b;
+        h2.wait = G->flags + c;
+        h2.pass = G->flags + G->flag_cap + c;
+        h2.wait_count = (uint32_t)ntiles_of((uint64_t)(uintptr_t)slot, ch.length, th);
+        h2.pass_count = (uint32_t)ntiles_of(d0 + ch.offset, ch.length, th);
+        h2.signal = (uint32_t*)G->done(dr);
+        h2.flags = mpk::TILE_SRC_MUTABLE | mpk::TILE_SIGNAL_BYTES;
+        append_tiles(tiles, 2 * round + 3, (uint64_t)(uintptr_t)slot, d0 + ch.offset, ch.length, th, h2);
+      }
       continue;
     }
     const int k = P.stage;
@@ -422,6 +470,37 @@ Entry* build_group_entry(mp_ctx* ctx, const std::string& key, const void* src, u
     e->progs.push_back(pr);
   }
   return e.release();
+}
+
+// A group host inbox: `bytes` of POSIX shared memory (created by its owner,
+// opened by every peer), pinned and mapped for this process's device.
+void map_host_inbox(const char* name, size_t bytes, bool create, uint8_t** host, uint8_t** dev) {
+  const int fd = shm_open(name, create ? (O_CREAT | O_EXCL | O_RDWR) : O_RDWR, 0600);
+  if (fd < 0) throw Error{MP_ERR_CUDA, std::string("shm_open ") + name + ": " + strerror(errno)};
+  if (create && ftruncate(fd, (off_t)bytes) != 0) {
+    close(fd);
+    shm_unlink(name);
+    throw Error{MP_ERR_CUDA, std::string("ftruncate host inbox: ") + strerror(errno)};
+  }
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) {
+    if (create) shm_unlink(name);
+    throw Error{MP_ERR_CUDA, std::string("mmap host inbox: ") + strerror(errno)};
+  }
+  const cudaError_t r = cudaHostRegister(p, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
+  if (r != cudaSuccess) {
+    munmap(p, bytes);
+    if (create) shm_unlink(name);
+    throw Error{MP_ERR_CUDA, std::string("cudaHostRegister host inbox: ") + cudaGetErrorString(r)};
+  }
+  CK(cudaHostGetDevicePointer((void**)dev, p, 0));
+  *host = (uint8_t*)p;
+}
+
+void unmap_host_inbox(uint8_t* host, size_t bytes) {
+  cudaHostUnregister(host);
+  munmap(host, bytes);
 }
 
 // Base address of the allocation holding `p` (driver entry point, resolved at
@@ -600,6 +679,12 @@ void mp_ctx_destroy(mp_ctx* ctx) {
     cudaFree(G->stage);
     cudaFree(G->flags);
     cudaFree(G->sync);
+    for (int q = 0; q < G->nranks; ++q)
+      if (G->peer_host[q]) unmap_host_inbox(G->peer_host[q], G->peer_host_cap[q]);
+    if (G->host) {
+      unmap_host_inbox(G->host, G->host_cap);
+      shm_unlink(G->host_name.c_str());
+    }
     delete G;
     ctx->group = nullptr;
   }
@@ -1301,6 +1386,9 @@ int mp_group_create(int32_t nranks, int32_t rank, int32_t device, uint64_t stage
   G->peer_sync.assign(nranks, nullptr);
   G->peer_flags.assign(nranks, nullptr);
   G->peer_stage_cap.assign(nranks, 0);
+  G->peer_host.assign(nranks, nullptr);
+  G->peer_host_dev.assign(nranks, nullptr);
+  G->peer_host_cap.assign(nranks, 0);
   try {
     CK(cudaSetDevice(device));
     CK(cudaMalloc(&G->stage, G->stage_cap));
@@ -1318,6 +1406,25 @@ int mp_group_create(int32_t nranks, int32_t rank, int32_t device, uint64_t stage
   GUARD_END
 }
 
+int mp_group_host_arena(mp_ctx* ctx, uint64_t bytes) {
+  GUARD_BEGIN
+  if (!ctx || !ctx->group) return fail(MP_ERR_VALUE, "not a group context");
+  GroupState* G = ctx->group;
+  if (bytes == 0) return fail(MP_ERR_VALUE, "host inbox size must be >= 1 byte");
+  if (G->host) return fail(MP_ERR_STATE, "the host inbox is already set up");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  DeviceGuard g;
+  CK(cudaSetDevice(ctx->phys[0].ordinal));
+  static std::atomic<unsigned> serial{0};
+  const std::string name = "/mpb200_" + std::to_string((long)getpid()) + "_" + std::to_string(G->rank) +
+                           "_" + std::to_string(serial++);
+  map_host_inbox(name.c_str(), bytes, true, &G->host, &G->host_dev);
+  G->host_cap = bytes;
+  G->host_name = name;
+  return MP_OK;
+  GUARD_END
+}
+
 int mp_group_export(const mp_ctx* ctx, uint8_t* blob) {
   GUARD_BEGIN
   if (!ctx || !ctx->group || !blob) return fail(MP_ERR_VALUE, "not a group context");
@@ -1331,6 +1438,8 @@ int mp_group_export(const mp_ctx* ctx, uint8_t* blob) {
   CK(cudaIpcGetMemHandle(&b.stage, G->stage));
   CK(cudaIpcGetMemHandle(&b.flags, G->flags));
   CK(cudaIpcGetMemHandle(&b.sync, G->sync));
+  b.host_cap = G->host_cap;
+  snprintf(b.host_name, sizeof b.host_name, "%s", G->host_name.c_str());
   memset(blob, 0, MP_GROUP_BLOB_BYTES);
   memcpy(blob, &b, sizeof b);
   return MP_OK;
@@ -1359,6 +1468,11 @@ int mp_group_import(mp_ctx* ctx, int32_t rank, const uint8_t* blob) {
   G->peer_sync[rank] = (uint8_t*)p;
   G->peer_stage_cap[rank] = b.stage_cap;
   G->flag_cap = std::min(G->flag_cap, (int)b.flag_cap);
+  if (b.host_cap && !G->peer_host[rank]) {
+    b.host_name[sizeof b.host_name - 1] = 0;
+    map_host_inbox(b.host_name, b.host_cap, false, &G->peer_host[rank], &G->peer_host_dev[rank]);
+    G->peer_host_cap[rank] = b.host_cap;
+  }
   return MP_OK;
   GUARD_END
 }

@@ -6,16 +6,19 @@ GPU.  Here:
 
 * `TransferGroup(topology)` creates this rank's group context
   (`mp_group_create`: relay staging arena, relay flags and a sync block in its
-  HBM), exports their IPC handles and maps every peer's (`mp_group_import`) —
-  one all-gather at construction;
+  HBM; `mp_group_host_arena`: a host inbox in POSIX shared memory, pinned and
+  mapped), exports their IPC handles / inbox name and maps every peer's
+  (`mp_group_import`) — one all-gather at construction;
 * `expose(tensor, owner)` shares one buffer's IPC handle (broadcast from its
   owner, opened once per process and cached: `mp_group_open`);
 * `transfer(src_buf, dst_buf, nbytes, config)` is collective: every rank
   calls it in the same order; the source rank's kernel pushes Direct and
-  hop1 tiles into peer memory over NVLink, each relay rank's kernel moves its
-  hop2 tiles, the destination rank's kernel waits until every byte landed
-  (its stream is then ordered after the data), other ranks only join the
-  device-side barrier that orders consecutive transfers.
+  hop1 tiles into peer memory over NVLink (relay staging, or the
+  destination's host inbox over PCIe for the host-staged path), each relay
+  rank's kernel moves its hop2 tiles, the destination rank's kernel moves
+  the host path's hop2 tiles and waits until every byte landed (its stream
+  is then ordered after the data), other ranks only join the device-side
+  barrier that orders consecutive transfers.
 
 Rendezvous logic (`exchange_blobs`, `share_buffer`, `roles`) is plain
 torch.distributed + planner code, covered by gloo tests on CPU.
@@ -56,8 +59,6 @@ def roles(topology: Topology, src: int, dst: int, config: PathConfig) -> dict[in
     for p in ps.paths:
         if p.kind == "gpu":
             out[p.stage.index] = "relay"
-        elif p.kind == "host":
-            raise ValueError("the host-staged path needs a single-process Engine")
     return out
 
 
@@ -73,7 +74,8 @@ class RemoteBuffer:
 
 class TransferGroup:
     def __init__(self, topology: Topology, device: int | None = None,
-                 stage_bytes: int = 512 << 20, flag_cap: int = 4096, group=None):
+                 stage_bytes: int = 512 << 20, flag_cap: int = 4096, group=None,
+                 host_bytes: int = 64 << 20):
         import torch
         import torch.distributed as dist
         self.pg = group
@@ -88,6 +90,8 @@ class TransferGroup:
         check(lib.mp_group_create(self.world, self.rank, self.device, stage_bytes, flag_cap,
                                   C.byref(self._ctx)))
         check(lib.mp_ctx_set_topology(self._ctx, topology._handle))
+        if host_bytes:
+            check(lib.mp_group_host_arena(self._ctx, host_bytes))
         blob = (C.c_uint8 * MP_GROUP_BLOB_BYTES)()
         check(lib.mp_group_export(self._ctx, blob))
         for q, b in enumerate(exchange_blobs(bytes(blob), group)):

@@ -69,7 +69,7 @@ def test_struct_layout_matches_c_compiler(tmp_path):
 
 
 def test_abi_version_and_error_text():
-    assert _lib.lib.mp_abi_version() == 3
+    assert _lib.lib.mp_abi_version() == 4
     h = ctypes.c_void_p()
     rc = _lib.lib.mp_topology_load(b"[device]\n0 accelerator\n1 gpu\n", b"t", ctypes.byref(h))
     assert rc == _lib.MP_ERR_TOPOLOGY

@@ -60,11 +60,13 @@ def test_every_rank_derives_the_same_plan_world3():
     _dist_util.run(_worker_plans, 3)
 
 
-def test_host_path_rejected_in_group_mode():
-    import pytest
-
+def test_host_path_roles_in_group_mode():
+    """The host-staged path adds no rank role: the sender writes the
+    destination's host inbox, the destination loads it back."""
     import paper_2604_22228_b200 as mp
     from paper_2604_22228_b200 import group
-    topo = mp.load_topology(mp.mesh_text("g", 2, 7.5e11, 1, 2e-6, 5.5e10, 1e-5, "full"))
-    with pytest.raises(ValueError, match="single-process"):
-        group.roles(topo, 0, 1, mp.PathConfig(host_path_enabled=True))
+    topo = mp.load_topology(mp.mesh_text("g", 3, 7.5e11, 1, 2e-6, 5.5e10, 1e-5, "full"))
+    assert group.roles(topo, 0, 1, mp.PathConfig(host_path_enabled=True)) == \
+        {0: "sender", 1: "receiver", 2: "idle"}
+    assert group.roles(topo, 0, 1, mp.PathConfig(2, host_path_enabled=True)) == \
+        {0: "sender", 1: "receiver", 2: "relay"}

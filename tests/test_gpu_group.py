@@ -18,23 +18,24 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-def _worker(rank, world, port, gpu_paths, graph, size, reps):
+def _worker(rank, world, port, gpu_paths, graph, size, reps, host=False, host_bw=5.5e10):
     import numpy as np
     import torch.distributed as dist
 
     import paper_2604_22228_b200 as mp
+    from oracle import planner as op
     from oracle import transfer as ot
     from paper_2604_22228_b200.group import TransferGroup
     _dist_util.init(rank, world, port)
     torch.cuda.set_device(0)
-    topo = mp.load_topology(mp.mesh_text("g", world, 7.5e11, 1, 2e-6, 5.5e10, 1e-5, "full"))
+    topo = mp.load_topology(mp.mesh_text("g", world, 7.5e11, 1, 2e-6, host_bw, 1e-5, "full"))
     grp = TransferGroup(topo, device=0, stage_bytes=64 << 20)
     src = torch.empty(size + 3, dtype=torch.uint8, device="cuda:0")[3:]  # unaligned on purpose
     dst = torch.empty(size, dtype=torch.uint8, device="cuda:0")
     sb = grp.expose(src, owner=0)
     db = grp.expose(dst, owner=1)
-    cfg = mp.PathConfig(num_gpu_paths=gpu_paths, max_chunks=4, graph_mode=graph,
-                        share_policy="equal")
+    cfg = mp.PathConfig(num_gpu_paths=gpu_paths, host_path_enabled=host, max_chunks=4,
+                        graph_mode=graph, share_policy="equal")
     for r in range(reps):
         data = ot.pattern(size, seed=100 + r)
         if rank == 0:
@@ -49,6 +50,11 @@ def _worker(rank, world, port, gpu_paths, graph, size, reps):
         if rank == 1:
             got = dst.cpu().numpy()
             assert np.array_equal(got, data), f"rep {r}: mismatch"
+            paths, chunks = grp.last_plan()
+            ochunks = op.make_chunk_plan([p["share"] for p in op.plan_paths(
+                op.parse_topology(mp.mesh_text("g", world, 7.5e11, 1, 2e-6, host_bw, 1e-5, "full")),
+                0, 1, gpu_paths, host, "equal")], size, 4)
+            assert [(c.path_index, c.offset, c.length, c.seq) for c in chunks] == ochunks
         dist.barrier()
     assert grp.role() == {0: 1, 1: 3}.get(rank, 2 if rank < gpu_paths + 1 else 0)
     grp.close()
@@ -59,3 +65,13 @@ def _worker(rank, world, port, gpu_paths, graph, size, reps):
 @pytest.mark.parametrize("graph", [False, True])
 def test_group_transfer(world, gpu_paths, graph):
     _dist_util.run(_worker, world, gpu_paths, graph, (4 << 20) + 12345, 3)
+
+
+@pytest.mark.parametrize("world,gpu_paths", [(2, 1), (3, 2)])
+@pytest.mark.parametrize("graph", [False, True])
+def test_group_transfer_with_host_path(world, gpu_paths, graph):
+    """Direct (+ relay) + host-staged in group mode: the sender's hop1 tiles
+    write the destination rank's host inbox (POSIX shm, pinned and mapped
+    in both processes) and release the chunk flag in the destination's HBM;
+    the destination's kernel loads the chunk back, then waits for every byte."""
+    _dist_util.run(_worker, world, gpu_paths, graph, (4 << 20) + 12345, 3, True)
