@@ -477,10 +477,14 @@ Entry* build_group_entry(mp_ctx* ctx, const std::string& key, const void* src, u
 void map_host_inbox(const char* name, size_t bytes, bool create, uint8_t** host, uint8_t** dev) {
   const int fd = shm_open(name, create ? (O_CREAT | O_EXCL | O_RDWR) : O_RDWR, 0600);
   if (fd < 0) throw Error{MP_ERR_CUDA, std::string("shm_open ") + name + ": " + strerror(errno)};
-  if (create && ftruncate(fd, (off_t)bytes) != 0) {
+  // reserve the pages now: a /dev/shm smaller than the inbox fails here
+  // (ENOSPC) instead of with SIGBUS when the pages are first touched
+  int fe = 0;
+  if (create && (ftruncate(fd, (off_t)bytes) != 0 || (fe = posix_fallocate(fd, 0, (off_t)bytes)) != 0)) {
+    const std::string why = strerror(fe ? fe : errno);
     close(fd);
     shm_unlink(name);
-    throw Error{MP_ERR_CUDA, std::string("ftruncate host inbox: ") + strerror(errno)};
+    throw Error{MP_ERR_CUDA, "host inbox of " + std::to_string(bytes) + " bytes in /dev/shm: " + why};
   }
   void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
   close(fd);
