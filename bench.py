@@ -169,7 +169,8 @@ class Clocks:
 def emit(out: dict) -> None:
     """The one result line (kept < 3 KB: optional keys are dropped if needed)."""
     line = json.dumps(out, separators=(",", ":"))
-    for k in ("notes", "errors", "multi_over_single", "reference_cpu_path_us", "graph"):
+    for k in ("notes", "errors", "multi_over_single_window8", "multi_over_single", "reference_cpu_path_us",
+              "graph"):
         if len(line) <= 3000:
             break
         out.pop(k, None)
@@ -421,6 +422,44 @@ def short_sweep(torch, eng, PathConfig, big, obig, stream, sizes, g, host, k, sd
     return rows
 
 
+def window_sweep(torch, eng, PathConfig, stream, sizes, g, host, k, W=8, sd=0, dd=1):
+    """Per size: single path vs the multi-path send when an osu_bw window of W
+    non-blocking messages (W distinct buffer pairs) is posted as ONE program
+    (Engine.prepare_many): each message's host round trip then overlaps the
+    other messages' direct copies instead of ending every message.  µs per
+    message = window time / W."""
+    rows = []
+    for s in sizes:
+        srcs = [torch.randint(0, 256, (s,), dtype=torch.uint8, device=f"cuda:{stream.device.index}")
+                for _ in range(W)]
+        dsts = [torch.empty_like(x) for x in srcs]
+        reps = max(10, min(200, (1 << 30) // (s * W)))
+        us = {}
+        for name, cfg in (("single", PathConfig(max_chunks=1, graph_mode=True)),
+                          ("multi", PathConfig(g, host, k, True))):
+            post = eng.prepare_many([(a, b, s, sd, dd) for a, b in zip(srcs, dsts)], cfg, stream=stream)
+            for _ in range(10):
+                post()
+            torch.cuda.synchronize()
+            best = None
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for _ in range(3):
+                e0.record(stream)
+                for _ in range(reps):
+                    post()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1) * 1e3 / (reps * W)
+                best = t if best is None else min(best, t)
+            eng.sync()
+            assert all(torch.equal(a, b) for a, b in zip(srcs, dsts)), "delivered bytes differ"
+            us[name] = best
+        rows.append({"bytes": s, "W": W, "single_us_per_msg": us["single"], "multi_us_per_msg": us["multi"],
+                     "ratio": us["single"] / us["multi"]})
+        del srcs, dsts
+    return rows
+
+
 def lifecycle(torch, eng, PathConfig, dev, stream, n=10000):
     """BASELINE config 5: 4 KiB-4 MiB, 10k iterations per arm: capture +
     instantiate per call, cached replay and per-call stream launch of a
@@ -569,6 +608,9 @@ def run_one(args) -> None:
                         [4 * MiB, 16 * MiB, 64 * MiB, 128 * MiB, 256 * MiB], g, host, k)
     detail["sweep_multi_vs_single"] = sweep
     out["multi_over_single"] = {f"{r['bytes'] >> 20}MiB": round(r["ratio"], 3) for r in sweep}
+    wins = window_sweep(torch, eng, PathConfig, stream, [4 * MiB, 8 * MiB, 16 * MiB, 64 * MiB], g, host, k)
+    detail["window_multi_vs_single"] = wins
+    out["multi_over_single_window8"] = {f"{r['bytes'] >> 20}MiB": round(r["ratio"], 3) for r in wins}
     lc = lifecycle(torch, eng, PathConfig, dev, stream)
     detail["lifecycle"] = lc
     out["replay_host_us"] = round(max(r["replay_host_us"] for r in lc), 2)
