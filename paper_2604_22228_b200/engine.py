@@ -446,11 +446,18 @@ class Engine:
         link, host = self.probe_bandwidths(nbytes, iters)
         return mesh_text(name, n, link, 1, 2e-6, host, 10e-6, "full")
 
-    def probe_node(self, nbytes: int = 256 << 20, iters: int = 5, name: str = "probed") -> str:
+    def probe_node(self, nbytes: int = 256 << 20, iters: int = 5, name: str = "probed",
+                   host_bytes: int = 8 << 20) -> str:
         """Measure every accelerator pair and host link of the context and
         write a reference-schema `.topo` (SURVEY §8c protocol: bandwidths with
         repr(), sublinks 1, so the planner parses back the identical doubles).
-        Pairs on the same physical devices are measured once."""
+        Pairs on the same physical devices are measured once.  A host link's
+        rate is the host-staged path's delivered rate as the engine runs it
+        (like `probe_bandwidths`), not the isolated PCIe rate: planned on the
+        isolated rate the staged path gets too large a share and multi-path
+        loses to single path (profiles/r02_exp_linkcap.jsonl: 0.74-0.89x at
+        128-512 MiB with a link-limited direct path, 1.02-1.06x on the
+        measured rate)."""
         n = len(self.topology.accelerators)
         pair_bw: dict[tuple[int, int], float] = {}
         host_bw: dict[int, float] = {}
@@ -466,8 +473,8 @@ class Engine:
         for d in range(n):
             phys = self.device_map[d]
             if phys not in host_bw:
-                m = self.measure_paths(d, d, nbytes, iters)
-                host_bw[phys] = min(m["d2h"], m["h2d"]) * 1e9
+                m = self.measure_paths(d, d, host_bytes, max(iters, 10))
+                host_bw[phys] = m["host_staged"] * 1e9
             lines.append(f"{d} {host_bw[phys]!r} 1e-05 full")
         return "\n".join(lines) + "\n"
 
