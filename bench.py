@@ -762,6 +762,7 @@ def run_node(args, rank: int, world: int) -> None:
         eng.sync()
         torch.cuda.synchronize()
         assert torch.equal(src.cpu(), dst.cpu()), "delivered bytes differ"
+        paths_, chunks_ = eng.last_plan()
         t, clocks = headline(torch, eng, cfg, src, dst, args, stream, 0)
         st = eng.stats()
         value = args.steps * W * size / t / 1e9
@@ -810,6 +811,18 @@ def run_node(args, rank: int, world: int) -> None:
         ingress = opt("ingress", ingress_probe) if world > 2 else None
         nvl = min(probe["direct_sm"] * g, ingress or float("inf"))
         R = nvl + pcie
+        r_kind = "R = min(paths x probed direct, probed dst ingress) + probed PCIe"
+        if ngpu < world:
+            # ranks share GPUs (loopback): every path copies through the same
+            # HBM — a direct byte costs one HBM copy, a relayed byte two, a
+            # host byte one read + one write — so R is the HBM copy rate over
+            # the plan's copy traffic per message byte
+            hbm, _ = peaks()
+            kinds = [p.kind for p in paths_]
+            per = {"direct": 1.0, "gpu": 2.0, "host": 1.0}
+            copies = sum(c.length * per.get(kinds[c.path_index], 1.0) for c in chunks_)
+            R = (hbm / 2) * size / copies
+            r_kind = "loopback (ranks share a GPU): HBM copy peak / 2 over the plan's HBM copies per byte"
 
         def relay_sweep():
             rows = []
@@ -827,7 +840,7 @@ def run_node(args, rank: int, world: int) -> None:
             "data": "synthetic (seeded random bytes)", "config": workload_config(args, world),
             "roofline": {"bound": "nvlink", "achieved": value, "peak": R, "unit": "GB/s",
                          "frac": value / R, "traffic": None,
-                         "peak_kind": "R = min(paths x probed direct, probed dst ingress) + probed PCIe"},
+                         "peak_kind": r_kind},
             "path_roofline": {"R_gbs": R, "direct_probe_gbs": probe["direct_sm"], "ingress_gbs": ingress,
                               "pcie_probed_gbs": pcie, "single_path_sm_gbs": gbs(t_sm),
                               "peer_memcpy_ce_gbs": gbs(t_ce),
