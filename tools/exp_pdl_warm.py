@@ -23,6 +23,14 @@ t0 = time.time()
 for p in range(int(os.environ.get("PASSES", "8"))):
     row = [round(measure_makespan(e, PathConfig(max_chunks=1, graph_mode=True), s, big[:s], out[:s], st, 50) * 1e6, 2)
            for s in sizes]
-    print(f"pass {p} t={time.time() - t0:.2f}s", row, flush=True)
+    # host µs per prepared 1 MiB send (enqueue only): is the slow phase host-bound?
+    go = e.prepare(big[:MiB], out[:MiB], MiB, PathConfig(max_chunks=1, graph_mode=True), stream=st,
+                   src_dev=0, dst_dev=1)
+    h0 = time.perf_counter()
+    for _ in range(50):
+        go()
+    host_us = (time.perf_counter() - h0) / 50 * 1e6
+    torch.cuda.synchronize()
+    print(f"pass {p} t={time.time() - t0:.3f}s host_us_per_send={host_us:.2f}", row, flush=True)
     if os.environ.get("CLEAR"):
         e.clear_cache()
