@@ -149,11 +149,20 @@ double now_us() {
   return duration<double, std::micro>(steady_clock::now().time_since_epoch()).count();
 }
 
+// cudaSetDevice costs ~55 ns of host time even to the current device,
+// cudaGetDevice ~25 ns (tools/host_api_cost.cu): switch only on a change
+inline void set_device(int ordinal) {
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != ordinal) CK(cudaSetDevice(ordinal));
+}
+
 struct DeviceGuard {
   int prev = -1;
   DeviceGuard() { cudaGetDevice(&prev); }
   ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
   }
 };
 
@@ -307,6 +316,16 @@ struct mp_ctx {
     std::list<Entry*>::iterator lru_pos;
     uint64_t epoch = 0;
   } last_many;
+  // the same for mp_send: the last single send's key bytes and entry
+  struct {
+    std::string key;
+    Entry* entry = nullptr;
+    std::list<Entry*>::iterator lru_pos;
+    uint64_t epoch = 0;
+  } last_one;
+  // mp_last_plan's source: copied from the entry only when it changes
+  const void* last_plan_of = nullptr;
+  uint64_t last_plan_epoch = ~0ull;
   cudaEvent_t last_done = nullptr;  // serialises sends issued on different streams
   void* last_stream = nullptr;
   bool have_last = false;

@@ -140,7 +140,7 @@ void enqueue(mp_ctx* ctx, Entry* e, cudaStream_t origin, bool timing, Trace* tr 
     return;
   }
   Phys& S = ctx->phys[e->src_phys];
-  CK(cudaSetDevice(S.ordinal));
+  set_device(S.ordinal);
   if (!tr && e->ce.empty() && e->progs.size() == 1 && e->progs[0].phys == e->src_phys) {
     // one kernel on the caller's device and nothing else: no fork/join, the
     // kernel goes straight onto the caller's stream (per-call launch ~= one
@@ -545,6 +545,16 @@ void check_sticky(const mp_ctx* ctx) {
   }
 }
 
+// mp_last_plan's copy of an entry's plan, refreshed only when the entry
+// changes (a resend of the same entry copies nothing)
+void remember_plan(mp_ctx* ctx, const Entry* e) {
+  if (ctx->last_plan_of == e && ctx->last_plan_epoch == ctx->cache_epoch) return;
+  ctx->last_paths = e->paths;
+  ctx->last_chunks = e->chunks;
+  ctx->last_plan_of = e;
+  ctx->last_plan_epoch = ctx->cache_epoch;
+}
+
 uint64_t timeout_ns(const mp_engine_opts& o) { return (uint64_t)o.wait_timeout_ms * 1000000ull; }
 
 // (Re)initialise a device's control block: zero counters and error word,
@@ -816,10 +826,31 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
   cudaStream_t user = (cudaStream_t)stream;
-  Entry* e = lookup_entry(ctx, src, dst, size, src_dev, dst_dev, *cfg, user);
+  // resend of the last single send (back-to-back messages on one buffer
+  // pair): the same key bytes and its entry still cached — a hit without
+  // the hash lookup (the key buffer is reused: a hit allocates nothing)
+  auto& lo = ctx->last_one;
+  thread_local std::string key;
+  key.clear();
+  append_key(key, src, dst, size, src_dev, dst_dev, *cfg);
+  Entry* e = nullptr;
+  if (lo.entry && lo.epoch == ctx->cache_epoch && lo.key == key) {
+    e = lo.entry;
+    ctx->lru.splice(ctx->lru.end(), ctx->lru, lo.lru_pos);
+    mp_send_stats& hs = ctx->stats;
+    hs.hit = 1;
+    hs.cache_hits++;
+    hs.creation_us = hs.construction_us = hs.instantiation_us = hs.plan_us = 0.0;
+  } else {
+    e = lookup_entry(ctx, src, dst, size, src_dev, dst_dev, *cfg, user, nullptr, &key);
+    lo.key = key;
+    lo.entry = e;
+    lo.lru_pos = ctx->index.find(key)->second;
+    lo.epoch = ctx->cache_epoch;
+  }
   mp_send_stats& st = ctx->stats;
   Phys& S = ctx->phys[e->src_phys];
-  CK(cudaSetDevice(S.ordinal));
+  set_device(S.ordinal);
   // serialise with a send issued on another stream (shared counters/arenas)
   if (ctx->have_last && ctx->last_stream != stream) CK(cudaStreamWaitEvent(user, ctx->last_done, 0));
   double t_launch = now_us();
@@ -842,8 +873,7 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
   st.kernel = MP_KERNEL_NONE;
   for (const Program& pr : e->progs)
     if (pr.phys == e->src_phys) st.kernel = kernel_of(ctx->opts, pr.kind, pr.peer);
-  ctx->last_paths = e->paths;
-  ctx->last_chunks = e->chunks;
+  remember_plan(ctx, e);
   return MP_OK;
   GUARD_END
 }
@@ -930,8 +960,7 @@ int mp_send_many(mp_ctx* ctx, const mp_xfer* xfers, int32_t n, const mp_config* 
   st.kernel = MP_KERNEL_NONE;
   for (const Program& pr : e->progs)
     if (pr.phys == e->src_phys) st.kernel = kernel_of(ctx->opts, pr.kind, pr.peer);
-  ctx->last_paths = e->paths;
-  ctx->last_chunks = e->chunks;
+  remember_plan(ctx, e);
   return MP_OK;
   GUARD_END
 }
@@ -1039,8 +1068,7 @@ int mp_send_trace(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_
     throw;
   }
   cleanup();
-  ctx->last_paths = e->paths;
-  ctx->last_chunks = e->chunks;
+  remember_plan(ctx, e);
   return MP_OK;
   GUARD_END
 }
@@ -1540,8 +1568,7 @@ int mp_group_send(mp_ctx* ctx, const void* src, uint32_t src_align, void* dst, u
   st.kernels = 1;
   st.ce_copies = 0;
   st.kernel = e->progs.empty() ? MP_KERNEL_NONE : kernel_of(ctx->opts, e->progs[0].kind, e->progs[0].peer);
-  ctx->last_paths = e->paths;
-  ctx->last_chunks = e->chunks;
+  remember_plan(ctx, e);
   return MP_OK;
   GUARD_END
 }
