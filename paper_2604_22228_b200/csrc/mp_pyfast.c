@@ -8,6 +8,7 @@
  * read with mp_last_error() on the same thread (engine.py re-raises). */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+#include <stddef.h>
 
 #include "mpb200.h"
 
@@ -48,43 +49,72 @@ typedef struct {
   int32_t sd, dd;
   const mp_config* cfg;
   void* stream;
-  PyObject* keep; /* objects that must outlive the binding (tensors, config, stream) */
+  PyObject* keep;     /* objects that must outlive the binding (tensors, config, stream) */
+  PyObject* on_error; /* on_error(rc) raises the mapped exception; NULL: return rc */
+  PyObject* weaklist; /* Engine keeps weak references to invalidate on close() */
 } BoundSend;
 
 static void bound_dealloc(BoundSend* self) {
+  if (self->weaklist) PyObject_ClearWeakRefs((PyObject*)self);
   Py_XDECREF(self->keep);
+  Py_XDECREF(self->on_error);
   Py_TYPE(self)->tp_free((PyObject*)self);
 }
 
+/* Success returns None with no Python-level work at all; a failure (or a
+ * binding invalidated by Engine.close(): rc = -1000, the context is never
+ * touched) goes to on_error, which maps the status to the reference's
+ * exception classes.  Without on_error the status is returned. */
 static PyObject* bound_call(BoundSend* self, PyObject* args, PyObject* kw) {
   (void)args;
   (void)kw;
-  int rc;
-  Py_BEGIN_ALLOW_THREADS
-  rc = mp_send(self->ctx, self->src, self->dst, self->size, self->sd, self->dd, self->cfg,
-               self->stream);
-  Py_END_ALLOW_THREADS
-  return PyLong_FromLong(rc);
+  int rc = -1000;
+  if (self->ctx) {
+    Py_BEGIN_ALLOW_THREADS
+    rc = mp_send(self->ctx, self->src, self->dst, self->size, self->sd, self->dd, self->cfg,
+                 self->stream);
+    Py_END_ALLOW_THREADS
+  }
+  if (!self->on_error) return PyLong_FromLong(rc);
+  if (rc == 0) Py_RETURN_NONE;
+  return PyObject_CallFunction(self->on_error, "i", rc);
 }
+
+static PyObject* bound_invalidate(BoundSend* self, PyObject* unused) {
+  (void)unused;
+  self->ctx = NULL;
+  Py_RETURN_NONE;
+}
+
+static PyMethodDef bound_methods[] = {
+    {"invalidate", (PyCFunction)bound_invalidate, METH_NOARGS,
+     "forget the context (Engine.close): later calls fail without touching it"},
+    {NULL, NULL, 0, NULL},
+};
 
 static PyTypeObject BoundSendType = {
     PyVarObject_HEAD_INIT(NULL, 0).tp_name = "_mpfast.BoundSend",
     .tp_basicsize = sizeof(BoundSend),
     .tp_dealloc = (destructor)bound_dealloc,
     .tp_call = (ternaryfunc)bound_call,
+    .tp_methods = bound_methods,
+    .tp_weaklistoffset = offsetof(BoundSend, weaklist),
     .tp_flags = Py_TPFLAGS_DEFAULT,
     .tp_doc = "a send bound to its arguments; call() -> MP_* status",
 };
 
 static PyObject* fast_bind(PyObject* self, PyObject* const* args, Py_ssize_t nargs) {
   (void)self;
-  if (nargs != 9) {
-    PyErr_SetString(PyExc_TypeError, "bind(ctx, src, dst, size, src_dev, dst_dev, cfg, stream, keep)");
+  if (nargs != 9 && nargs != 10) {
+    PyErr_SetString(PyExc_TypeError,
+                    "bind(ctx, src, dst, size, src_dev, dst_dev, cfg, stream, keep[, on_error])");
     return NULL;
   }
   BoundSend* b = PyObject_New(BoundSend, &BoundSendType);
   if (!b) return NULL;
   b->keep = NULL;
+  b->on_error = NULL;
+  b->weaklist = NULL;
   b->ctx = (mp_ctx*)PyLong_AsVoidPtr(args[0]);
   b->src = PyLong_AsVoidPtr(args[1]);
   b->dst = PyLong_AsVoidPtr(args[2]);
@@ -101,6 +131,10 @@ static PyObject* fast_bind(PyObject* self, PyObject* const* args, Py_ssize_t nar
   b->dd = (int32_t)dd;
   Py_INCREF(args[8]);
   b->keep = args[8];
+  if (nargs == 10 && args[9] != Py_None) {
+    Py_INCREF(args[9]);
+    b->on_error = args[9];
+  }
   return (PyObject*)b;
 }
 

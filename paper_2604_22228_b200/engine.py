@@ -18,6 +18,7 @@ relay flags included — on a single B200.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass
 
 from . import _lib, _mpfast
@@ -60,6 +61,14 @@ def _torch():
     return torch
 
 
+def _raise_status(rc: int) -> None:
+    """Error path of a prepared send (_mpfast.BoundSend): map an MP_* status
+    to the reference's exception classes; -1000 = used after Engine.close()."""
+    if rc == -1000:
+        raise EngineError("prepared send used after Engine.close()")
+    check(rc)
+
+
 class Engine:
     """A transfer context over `n_logical` accelerators of `topology`."""
 
@@ -74,6 +83,7 @@ class Engine:
             raise ValueError(f"device_map has {len(device_map)} entries for {n} accelerators")
         self.topology = topology
         self.device_map = list(device_map)
+        self._bindings: list = []  # weak refs to prepared sends (invalidated by close())
         arr = (C.c_int32 * n)(*self.device_map)
         self._ctx = C.c_void_p()
         check(lib.mp_ctx_create(n, arr, C.byref(self._ctx)))
@@ -89,6 +99,10 @@ class Engine:
         return cls(topo, [device] * n_logical)
 
     def close(self):
+        for ref in getattr(self, "_bindings", ()):
+            b = ref()
+            if b is not None:
+                b.invalidate()
         if getattr(self, "_ctx", None):
             self._ctx_addr = 0
             lib.mp_ctx_destroy(self._ctx)
@@ -257,19 +271,14 @@ class Engine:
         outlive the engine."""
         config, nbytes, src_dev, dst_dev, handle = self._resolve(src, dst, nbytes, config, stream,
                                                                  src_dev, dst_dev)
-        ctx = self._ctx_addr
-        bound = _mpfast.bind(ctx, src.data_ptr(), dst.data_ptr(), nbytes, src_dev, dst_dev,
-                             config.abi_addr(), handle or 0, (src, dst, config, stream))
-        engine = self
-
-        def launch() -> None:
-            if engine._ctx_addr != ctx:  # closed engine: never touch a freed context
-                raise EngineError("prepared send used after Engine.close()")
-            rc = bound()
-            if rc:
-                check(rc)
-        launch.bound = bound  # the raw C callable (returns the MP_* status)
-        return launch
+        bound = _mpfast.bind(self._ctx_addr, src.data_ptr(), dst.data_ptr(), nbytes, src_dev, dst_dev,
+                             config.abi_addr(), handle or 0, (src, dst, config, stream), _raise_status)
+        # the call itself is C (None on success); Engine.close() invalidates
+        # every binding so a stale one never touches the freed context
+        if len(self._bindings) > 4096:
+            self._bindings = [r for r in self._bindings if r() is not None]
+        self._bindings.append(weakref.ref(bound))
+        return bound
 
     def _xfers(self, transfers, stream):
         """(mp_xfer array, stream handle) for send_many / prepare_many."""

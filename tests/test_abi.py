@@ -5,6 +5,8 @@ import ctypes
 import os
 import re
 
+import pytest
+
 from paper_2604_22228_b200 import _lib
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -134,3 +136,21 @@ def test_build_module_runs_as_documented():
                         "sys.exit(0 if m._lib.lib is not None and m.Engine else 1)"],
                        cwd=ROOT, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_bound_send_invalidated_never_touches_the_context():
+    """A prepared send (`_mpfast.BoundSend`) invalidated by Engine.close()
+    raises through its error hook without calling mp_send (the context
+    pointer here is a dummy that would crash if used)."""
+    from paper_2604_22228_b200 import _mpfast
+    from paper_2604_22228_b200._lib import EngineError
+    from paper_2604_22228_b200.engine import _raise_status
+    b = _mpfast.bind(0xDEAD0000, 1, 2, 16, 0, 1, 0, 0, (), _raise_status)
+    b.invalidate()
+    with pytest.raises(EngineError, match="after Engine.close"):
+        b()
+    raw = _mpfast.bind(0xDEAD0000, 1, 2, 16, 0, 1, 0, 0, ())
+    raw.invalidate()
+    assert raw() == -1000  # no hook: the status is returned
+    import weakref
+    assert weakref.ref(b)() is b
