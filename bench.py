@@ -722,9 +722,15 @@ def run_node(args, rank: int, world: int) -> None:
     g, host, k = plan_shape(args, world)
     text = open(topo_file(world)).read()
     out = None
+    # testing knob (loopback only): lower the logical GPUs as separate devices
+    # — system-scope flags, host chunks as hop1 / hop2 tiles, the peer (LDG/STG)
+    # launch path — so the real multi-GPU lowering runs end to end on one GPU
+    emulate = os.environ.get("MP_EMULATE_PEERS") == "1" and ngpu < world
     if rank == 0:
         torch.cuda.set_device(0)
         eng = Engine(load_topology(text), dmap)
+        if emulate:
+            eng.configure(fault_inject=2, tma_peer=-1)
         # Everything but the headline is optional evidence: a failure there
         # is reported in the line ("errors") and never costs the headline.
         errors = {}
@@ -774,7 +780,7 @@ def run_node(args, rank: int, world: int) -> None:
 
         def ce_arm():
             ce = Engine(load_topology(text), dmap)
-            ce.configure(direct="ce")
+            ce.configure(direct="ce", **({"fault_inject": 2, "tma_peer": -1} if emulate else {}))
             try:
                 return time_send(torch, ce, PathConfig(max_chunks=1, graph_mode=False), src, dst, size, 20,
                                  stream)
@@ -849,6 +855,8 @@ def run_node(args, rank: int, world: int) -> None:
                     if e2e else {"unavailable": errors.get("e2e", "")}),
             "gpu_launches": args.steps * W * st.kernels, "clocks": clocks, "planning": planning,
         }
+        if emulate:
+            out["config"]["emulated_peers"] = "fault_inject=2, tma_peer=-1 (testing knob: cross-device lowering in loopback)"
         if errors:
             out["errors"] = errors
         eng.close()
