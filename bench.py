@@ -796,12 +796,13 @@ def run_node(args, rank: int, world: int) -> None:
                     {"direct_sm": float("nan"), "d2h": float("nan"), "h2d": float("nan")})
         pcie = min(probe["d2h"], probe["h2d"])
 
-        def ingress_probe():
-            peers = [d for d in range(world) if d != 1]
-            bufs = [(torch.empty(size // 2, dtype=torch.uint8, device=f"cuda:{dmap[d]}"),
-                     torch.empty(size // 2, dtype=torch.uint8, device=f"cuda:{dmap[1]}"), d)
-                    for d in peers]
-            post = eng.prepare_many([(s_, d_, None, d, 1) for s_, d_, d in bufs],
+        def fan_probe(pairs):
+            """GB/s of concurrent direct copies over `pairs` [(src, dst)] as ONE
+            program (one kernel per source device)."""
+            bufs = [(torch.empty(size // 2, dtype=torch.uint8, device=f"cuda:{dmap[a]}"),
+                     torch.empty(size // 2, dtype=torch.uint8, device=f"cuda:{dmap[b]}"), a, b)
+                    for a, b in pairs]
+            post = eng.prepare_many([(s_, d_, None, a, b) for s_, d_, a, b in bufs],
                                     PathConfig(1, False, 1, True), stream=stream)
             for _ in range(3):
                 post()
@@ -813,11 +814,14 @@ def run_node(args, rank: int, world: int) -> None:
             e1.record(stream)
             torch.cuda.synchronize()
             eng.sync()
-            return 10 * len(peers) * (size // 2) / (e0.elapsed_time(e1) / 1e3) / 1e9
-        ingress = opt("ingress", ingress_probe) if world > 2 else None
-        nvl = min(probe["direct_sm"] * g, ingress or float("inf"))
+            return 10 * len(pairs) * (size // 2) / (e0.elapsed_time(e1) / 1e3) / 1e9
+        # the destination's ingress with every other GPU writing it, and the
+        # source's egress writing every other GPU (R's caps)
+        ingress = opt("ingress", lambda: fan_probe([(d, 1) for d in range(world) if d != 1])) if world > 2 else None
+        egress = opt("egress", lambda: fan_probe([(0, d) for d in range(1, world)])) if world > 2 else None
+        nvl = min(probe["direct_sm"] * g, ingress or float("inf"), egress or float("inf"))
         R = nvl + pcie
-        r_kind = "R = min(paths x probed direct, probed dst ingress) + probed PCIe"
+        r_kind = "R = min(paths x probed direct, probed dst ingress, probed src egress) + probed PCIe"
         if ngpu < world:
             # ranks share GPUs (loopback): every path copies through the same
             # HBM — a direct byte costs one HBM copy, a relayed byte two, a
@@ -848,6 +852,7 @@ def run_node(args, rank: int, world: int) -> None:
                          "frac": value / R, "traffic": None,
                          "peak_kind": r_kind},
             "path_roofline": {"R_gbs": R, "direct_probe_gbs": probe["direct_sm"], "ingress_gbs": ingress,
+                              "egress_gbs": egress,
                               "pcie_probed_gbs": pcie, "single_path_sm_gbs": gbs(t_sm),
                               "peer_memcpy_ce_gbs": gbs(t_ce),
                               "multi_streamed_gbs": gbs(t_stream), "relay_sweep": relays},

@@ -138,3 +138,22 @@ def test_ingress_probe_all_peers_to_one_gpu():
     for s, t, _ in bufs:
         assert torch.equal(s.cpu(), t.cpu())
     eng.close()
+
+
+@needs2
+def test_egress_probe_one_gpu_to_all_peers():
+    """The roofline's B_egress probe (bench.py N > 1): GPU0 writes every
+    other GPU at once as ONE program; the bytes land exactly."""
+    from paper_2604_22228_b200 import PathConfig
+    n = min(_ngpu(), 8)
+    eng, _ = _engine(n)
+    size = 32 * MiB + 5
+    bufs = []
+    for d in range(1, n):
+        s = torch.randint(0, 256, (size,), dtype=torch.uint8, device="cuda:0")
+        bufs.append((s, torch.zeros(size, dtype=torch.uint8, device=f"cuda:{d}"), d))
+    eng.send_many([(s, t, None, 0, d) for s, t, d in bufs], PathConfig(1, False, 1, True))
+    eng.sync()
+    for s, t, _ in bufs:
+        assert torch.equal(s.cpu(), t.cpu())
+    eng.close()
