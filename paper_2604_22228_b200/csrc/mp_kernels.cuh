@@ -905,8 +905,14 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
 
 // Receiver side of a group transfer: wait until `expected` bytes have landed
 // (direct and hop2 tiles add their sizes to *done), re-arm, finish the barrier.
+// ONE thread does the protocol (the kernels launch as one warp): with every
+// thread of the warp in it, each bumped this rank's generation — 32 per
+// transfer — so a sender ran ahead and its bytes landed before the previous
+// wait re-armed the counter (a back-to-back timeout found in round 2,
+// tests/test_gpu_group.py::test_group_back_to_back_transfers).
 __global__ void group_recv_kernel(GroupSync gsync, unsigned long long* done,
                                   unsigned long long expected, Ctl* ctl) {
+  if (threadIdx.x != 0) return;
   group_wait(gsync, ctl);
   const uint64_t t0 = globaltimer();
   while (true) {
@@ -926,6 +932,7 @@ __global__ void group_recv_kernel(GroupSync gsync, unsigned long long* done,
 
 // A rank with no part in a group transfer still takes part in its barrier.
 __global__ void group_noop_kernel(GroupSync gsync, Ctl* ctl) {
+  if (threadIdx.x != 0) return;  // one thread: one generation bump per transfer
   group_wait(gsync, ctl);
   group_done(gsync);
 }

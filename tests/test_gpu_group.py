@@ -75,3 +75,58 @@ def test_group_transfer_with_host_path(world, gpu_paths, graph):
     in both processes) and release the chunk flag in the destination's HBM;
     the destination's kernel loads the chunk back, then waits for every byte."""
     _dist_util.run(_worker, world, gpu_paths, graph, (4 << 20) + 12345, 3, True)
+
+
+def _b2b_worker(rank, world, port, gpu_paths, host, graph):
+    import time
+
+    import numpy as np
+    import torch.distributed as dist
+
+    import paper_2604_22228_b200 as mp
+    from oracle import transfer as ot
+    from paper_2604_22228_b200.group import TransferGroup
+    _dist_util.init(rank, world, port)
+    torch.cuda.set_device(0)
+    size = (8 << 20) + 77
+    topo = mp.load_topology(mp.mesh_text("g", world, 7.5e11, 1, 2e-6, 5.5e10, 1e-5, "full"))
+    grp = TransferGroup(topo, device=0, stage_bytes=64 << 20)
+    grp.configure(wait_timeout_ms=2000)
+    src = torch.empty(size, dtype=torch.uint8, device="cuda:0")
+    dst = torch.empty(size, dtype=torch.uint8, device="cuda:0")
+    sb, db = grp.expose(src, owner=0), grp.expose(dst, owner=1)
+    cfg = mp.PathConfig(num_gpu_paths=gpu_paths, host_path_enabled=host, max_chunks=4, graph_mode=graph)
+    data = ot.pattern(size, seed=5)
+    if rank == 0:
+        src.copy_(torch.from_numpy(data))
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream(device=0)
+    grp.transfer(sb, db, size, cfg, stream=stream)  # first: capture / build on every rank
+    stream.synchronize()
+    grp.sync()
+    dist.barrier()
+    # every rank but the sender enqueues late, so the sender's kernels must
+    # wait at the device barrier (one generation per rank per transfer)
+    if rank != 0:
+        time.sleep(0.2)
+    for _ in range(8):
+        grp.transfer(sb, db, size, cfg, stream=stream)
+    stream.synchronize()
+    grp.sync()  # raises if any wait timed out
+    if rank == 1:
+        assert np.array_equal(dst.cpu().numpy(), data)
+    dist.barrier()
+    grp.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,gpu_paths,host", [(2, 1, False), (2, 1, True), (3, 2, False)])
+@pytest.mark.parametrize("graph", [False, True])
+def test_group_back_to_back_transfers(world, gpu_paths, host, graph):
+    """Transfers enqueued back to back with no host sync, the receiver (and
+    relay) late: the device barrier alone orders them.  Regression: the
+    receiver's and idle ranks' one-warp barrier kernels once bumped their
+    generation once per THREAD, so the sender ran ahead, its bytes landed
+    before the previous wait re-armed the counter, and the next wait timed
+    out."""
+    _dist_util.run(_b2b_worker, world, gpu_paths, host, graph)
