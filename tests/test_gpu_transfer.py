@@ -412,3 +412,29 @@ def test_chained_sends_keep_stream_order(pdl):
         assert eng.stats().kernel.startswith(want)
         assert bool((b == 39).all()) and bool((c == 39).all())
     eng.close()
+
+
+@pytest.mark.parametrize("host,graph", [(False, True), (True, True), (True, False)])
+def test_recv_orders_a_consumer_stream_after_the_send(host, graph):
+    """Engine.recv (mp_wait): a consumer on ANOTHER stream that reads dst
+    right after recv sees the delivered bytes — the tail of a 256 MiB
+    message, the last bytes a multi-path send writes — never stale ones."""
+    from paper_2604_22228_b200 import PathConfig
+    eng, _ = _engine(2)
+    n = 256 * MiB + 5
+    src = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0")
+    dst = torch.empty_like(src)
+    tail = torch.empty(MiB, dtype=torch.uint8, device="cuda:0")
+    a, b = torch.cuda.Stream(), torch.cuda.Stream()
+    cfg = PathConfig(host_path_enabled=host, max_chunks=8, graph_mode=graph)
+    for r in range(4):
+        dst.fill_(r)
+        torch.cuda.synchronize()
+        eng.send(src, dst, n, cfg, stream=a, src_dev=0, dst_dev=1)
+        eng.recv(dst, stream=b)
+        with torch.cuda.stream(b):
+            tail.copy_(dst[-MiB:])
+        b.synchronize()
+        assert torch.equal(tail, src[-MiB:]), f"round {r}: the consumer read before the send finished"
+    eng.sync()
+    eng.close()
