@@ -438,3 +438,30 @@ def test_recv_orders_a_consumer_stream_after_the_send(host, graph):
         assert torch.equal(tail, src[-MiB:]), f"round {r}: the consumer read before the send finished"
     eng.sync()
     eng.close()
+
+
+def test_eviction_under_multi_stream_churn():
+    """cache_capacity 2 with 8 buffer pairs sent round-robin from 3 streams:
+    every send after the first two evicts an entry whose graph may still be
+    replaying on another stream.  Each pair's last delivery must be exact."""
+    from paper_2604_22228_b200 import PathConfig
+    eng, _ = _engine(3)
+    cfgs = [PathConfig(1, True, 4, True, cache_capacity=2), PathConfig(2, True, 3, True, cache_capacity=2),
+            PathConfig(1, False, 2, False, cache_capacity=2)]
+    pairs = []
+    for i in range(8):
+        n = (2 + i) * MiB + 13 * i
+        data = ot.pattern(n, seed=40 + i)
+        pairs.append((torch.from_numpy(data).to("cuda:0"), torch.empty(n, dtype=torch.uint8, device="cuda:0"),
+                      n, data))
+    streams = [torch.cuda.Stream() for _ in range(3)]
+    for r in range(5):
+        for i, (src, dst, n, _) in enumerate(pairs):
+            k = (r + i) % 3
+            eng.send(src, dst, n, cfgs[k], stream=streams[k], src_dev=0, dst_dev=1)
+    torch.cuda.synchronize()
+    eng.sync()
+    assert eng.stats().cache_evictions >= 30
+    for src, dst, n, data in pairs:
+        assert np.array_equal(dst.cpu().numpy(), data), f"{n} B"
+    eng.close()
