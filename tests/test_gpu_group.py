@@ -120,7 +120,7 @@ def _b2b_worker(rank, world, port, gpu_paths, host, graph):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,gpu_paths,host", [(2, 1, False), (2, 1, True), (3, 2, False)])
+@pytest.mark.parametrize("world,gpu_paths,host", [(2, 1, False), (2, 1, True), (3, 2, False), (4, 3, True)])
 @pytest.mark.parametrize("graph", [False, True])
 def test_group_back_to_back_transfers(world, gpu_paths, host, graph):
     """Transfers enqueued back to back with no host sync, the receiver (and
