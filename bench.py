@@ -559,12 +559,17 @@ def run_one(args) -> None:
     t_ce = time_send(torch, ce, PathConfig(max_chunks=1, graph_mode=False), src, dst, size, 40, stream)
     ce.close()
 
-    # dominant kernel: CUDA events around back-to-back launches of this
-    # send's program on its own stream (mp_kernel_bench)
+    # dominant kernel: every headline send is ONE launch of it on the
+    # caller's stream (st.kernels == 1, no copy-engine ops), so its average
+    # launch duration is the timed region's CUDA-event time over the K*W
+    # launches; cross-check: CUDA events around back-to-back ORDINARY
+    # launches of the same program (mp_kernel_bench; no PDL overlap)
+    launches = args.steps * W * st.kernels
+    kms_step = t * 1e3 / launches if st.kernels == 1 and st.ce_copies == 0 else None
     kms = eng.kernel_bench(src, dst, size, PathConfig(g, host, k, False), 0, 1,
                            reps=max(10, args.steps))
     k_alg = 2 * direct_bytes  # HBM read + write of the direct share
-    achieved = k_alg / (kms / 1e3) / 1e9
+    achieved = k_alg / ((kms_step or kms) / 1e3) / 1e9
     R = hbm_peak / 2 + pcie  # SURVEY §8d in loopback: HBM copy + PCIe
 
     out = {
@@ -574,7 +579,8 @@ def run_one(args) -> None:
         "data": "synthetic (seeded random bytes, seed 20261017)", "config": workload_config(args, 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": ncu_traffic(),
-                     "kernel": st.kernel.split(" ")[0], "kernel_ms": kms,
+                     "kernel": st.kernel.split(" ")[0], "kernel_ms": kms_step or kms,
+                     "kernel_ms_isolated": kms,
                      "alg_bytes_per_launch": k_alg, "peak_kind": peak_kind},
         "path_roofline": {"R_gbs": R, "frac": value / R, "hbm_copy_gbs": hbm_peak / 2,
                           "pcie_probed_gbs": pcie, "host_bw_planning_gbs": host_rate(text) / 1e9,
