@@ -29,7 +29,7 @@ def test_product_never_imports_the_oracle():
 def test_package_refuses_to_import_without_the_cuda_library(tmp_path):
     dst = tmp_path / "paper_2604_22228_b200"
     shutil.copytree(PKG, dst, ignore=shutil.ignore_patterns("*.so", "_build", "__pycache__"))
-    env = dict(os.environ, PYTHONPATH=str(tmp_path), MP_LIB_PATH="")
+    env = dict(os.environ, PYTHONPATH=str(tmp_path))
     out = subprocess.run([sys.executable, "-c", "import paper_2604_22228_b200"], cwd=str(tmp_path), env=env,
                          capture_output=True, text=True, timeout=300)
     assert out.returncode != 0, "imported without libmpb200.so: a silent fallback"
