@@ -26,6 +26,20 @@ constexpr uint64_t kRoundtripMaxBytes = 64 << 10;
 // (the relay's table holds only hop2 tiles).
 constexpr uint64_t kHop2Delay = 1;
 
+// Helper-warp roundtrips of messages from this size on end with a
+// system-scope fence (mpk::TILE_FENCE): the host writes retire inside the
+// direct stream instead of in the grid-completion flush the next
+// (programmatic-dependent) launch waits for.  Below it the fence outlasts
+// the message's copy.  Direct + host k=8 over single path, fence off -> on
+// (tools/exp_rtfence.py, profiles/r02_exp_rtfence.jsonl): 8 MiB 0.82 ->
+// 0.65, 16 MiB 0.81 -> 0.83-0.85, 24 MiB 0.82 -> 0.96, 32 MiB 0.97 -> 0.99,
+// 48-92 MiB 0.99 -> 1.00.  MP_RT_FENCE_MIN overrides it (experiments).
+constexpr uint64_t kRoundtripFenceMinBytes = 16ull << 20;
+inline uint64_t rt_fence_min_bytes() {
+  const char* e = std::getenv("MP_RT_FENCE_MIN");
+  return e ? (uint64_t)std::strtoull(e, nullptr, 10) : kRoundtripFenceMinBytes;
+}
+
 // cudaMemcpy2D pitches stay below the device's maximum pitch (2^31 - 1 class)
 constexpr uint64_t kMaxCopyPitch = 1ull << 30;
 
@@ -535,7 +549,7 @@ class Lowering {
       rt.dst = d0 + ch.offset;
       rt.stage = slot;
       rt.len = ch.length;
-      rt.flags = mpk::TILE_ROUNDTRIP;
+      rt.flags = mpk::TILE_ROUNDTRIP | (x.size >= rt_fence_min_bytes() ? mpk::TILE_FENCE : 0u);
       rt.node = n_a;  // hop2 is n_a + 1 == n_b
       // hop1 writes whole 128-byte lines into the slot (the chunk widened
       // to its source lines, clipped to the message): a partial-line PCIe

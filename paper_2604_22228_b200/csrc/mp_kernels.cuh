@@ -48,6 +48,12 @@ enum : uint32_t {
   // signal / wait at GPU scope: producer and consumer tiles run on the same
   // device (a relay or host chunk in loopback), so no system-scope release
   TILE_SCOPE_GPU = 8u,
+  // a helper-warp roundtrip ends with a system-scope fence (messages long
+  // enough for the fence to finish inside the direct stream): the host
+  // writes then retire before the grid completes, instead of in its flush,
+  // which a programmatic-dependent next launch waits for (~0.7 us at
+  // 32-64 MiB, tools/hoststore_probe.cu)
+  TILE_FENCE = 16u,
 };
 
 // Cross-process ordering of consecutive group transfers (multi-process mode):
@@ -773,7 +779,7 @@ __global__ void __launch_bounds__(256) transfer_kernel(const Tile* __restrict__ 
         const Tile t = tiles[ntiles + j];
         if (htid == 0) trace_start(trace, t.node);
         if (t.flags & TILE_ROUNDTRIP) {
-          roundtrip<UNROLL>(t, htid, hnt, 1, trace, htid == 0, false);
+          roundtrip<UNROLL>(t, htid, hnt, 1, trace, htid == 0, (t.flags & TILE_FENCE) != 0);
           asm volatile("bar.sync 1, %0;" ::"r"(hnt) : "memory");
           if (htid == 0) trace_end(trace, t.node + 1);
         } else {  // hop1 to host memory (the destination GPU's kernel runs hop2)
