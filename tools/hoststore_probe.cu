@@ -9,6 +9,9 @@
 //   8 st.release.sys of the last vector (release at system scope)
 //   9 st.global, fence.sc.sys, barrier, read back (fence BEFORE hop2)
 //  10 st.global, barrier, read back, fence.sc.sys (fence after hop2)
+//  12-14: the roundtrip on an EXTRA CTA (grid + 1) that does no copy work:
+//  12 no fence, 13 fence.sc.sys after the stores (before the read back),
+//  14 fence.sc.sys after the read back
 // Prints: bytes hb mode us_per_kernel
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o hoststore_probe hoststore_probe.cu
 #include <cuda_runtime.h>
@@ -50,6 +53,35 @@ __device__ __forceinline__ void st_mode(int4* p, const int4& v, int mode) {
 __global__ void __launch_bounds__(256) copyk(const int4* __restrict__ s, int4* __restrict__ d, size_t n16,
                                              int4* host, int4* back, int hn16, int mode) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (mode >= 12) {
+    if (blockIdx.x == gridDim.x - 1) {  // the extra CTA: the roundtrip only
+      const int t = threadIdx.x, nt = blockDim.x;
+      for (int i = t; i < hn16; i += nt) st_mode(host + i, s[i], 1);
+      if (mode == 13) asm volatile("fence.sc.sys;" ::: "memory");
+      __syncthreads();
+      for (int i = t; i < hn16; i += nt) {
+        int4 v;
+        asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(host + i));
+        back[i] = v;
+      }
+      if (mode == 14) asm volatile("fence.sc.sys;" ::: "memory");
+    } else {
+      const size_t stride = (size_t)(gridDim.x - 1) * blockDim.x;
+      size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+      for (; i + 7 * stride < n16; i += 8 * stride) {
+        int4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = s[i + u * stride];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) d[i + u * stride] = v[u];
+      }
+      for (; i < n16; i += stride) d[i] = s[i];
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    return;
+  }
   if (blockIdx.x == 0 && threadIdx.x >= 32 && mode > 0) {
     const int t = threadIdx.x - 32, nt = blockDim.x - 32;
     for (int i = t; i < hn16; i += nt) st_mode(host + i, s[i], mode);
@@ -100,13 +132,13 @@ int main() {
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  const size_t sizes[] = {4ull << 20, 8ull << 20, 16ull << 20, 32ull << 20, 64ull << 20};
+  const size_t sizes[] = {4ull << 20, 8ull << 20, 16ull << 20, 32ull << 20};
   for (int rep = 0; rep < 2; ++rep)
     for (size_t bytes : sizes)
       for (int hb : {512, 4096})
-        for (int mode : {0, 1, 5, 7, 9, 10}) {
+        for (int mode : {0, 1, 5, 7, 9, 10, 12, 13, 14}) {
           cudaLaunchConfig_t lc = {};
-          lc.gridDim = dim3(148 * 4);
+          lc.gridDim = dim3(148 * 4 + (mode >= 12 ? 1 : 0));
           lc.blockDim = dim3(256);
           lc.stream = st;
           cudaLaunchAttribute a[1];
