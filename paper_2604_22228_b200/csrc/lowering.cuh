@@ -549,7 +549,12 @@ class Lowering {
       rt.dst = d0 + ch.offset;
       rt.stage = slot;
       rt.len = ch.length;
-      rt.flags = mpk::TILE_ROUNDTRIP | (x.size >= rt_fence_min_bytes() ? mpk::TILE_FENCE : 0u);
+      // fence when the source device's whole program (every transfer of a
+      // send_many window) is long enough to hide it
+      uint64_t on_src = 0;
+      for (const Xfer& y : xs_)
+        if (phys_of(y.sd) == sp) on_src += y.size;
+      rt.flags = mpk::TILE_ROUNDTRIP | (on_src >= rt_fence_min_bytes() ? mpk::TILE_FENCE : 0u);
       rt.node = n_a;  // hop2 is n_a + 1 == n_b
       // hop1 writes whole 128-byte lines into the slot (the chunk widened
       // to its source lines, clipped to the message): a partial-line PCIe
