@@ -32,9 +32,10 @@ constexpr uint64_t kHop2Delay = 1;
 // (programmatic-dependent) launch waits for.  Below it the fence outlasts
 // the message's copy.  Direct + host k=8 over single path, fence off -> on
 // (tools/exp_rtfence.py, profiles/r02_exp_rtfence.jsonl): 8 MiB 0.82 ->
-// 0.65, 16 MiB 0.81 -> 0.83-0.85, 24 MiB 0.82 -> 0.96, 32 MiB 0.97 -> 0.99,
-// 48-92 MiB 0.99 -> 1.00.  MP_RT_FENCE_MIN overrides it (experiments).
-constexpr uint64_t kRoundtripFenceMinBytes = 16ull << 20;
+// 0.65, 16 MiB 0.78-0.85 -> 0.74-0.85 (box-dependent), 20 MiB even,
+// 24 MiB 0.82 -> 0.96, 32 MiB 0.97 -> 0.99, 48-92 MiB 0.99 -> 1.00.
+// MP_RT_FENCE_MIN overrides it (experiments).
+constexpr uint64_t kRoundtripFenceMinBytes = 20ull << 20;
 inline uint64_t rt_fence_min_bytes() {
   const char* e = std::getenv("MP_RT_FENCE_MIN");
   return e ? (uint64_t)std::strtoull(e, nullptr, 10) : kRoundtripFenceMinBytes;
