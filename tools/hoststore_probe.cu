@@ -9,6 +9,8 @@
 //   8 st.release.sys of the last vector (release at system scope)
 //   9 st.global, fence.sc.sys, barrier, read back (fence BEFORE hop2)
 //  10 st.global, barrier, read back, fence.sc.sys (fence after hop2)
+//  15 hop1 as a TMA bulk store (smem -> host, cp.async.bulk + wait_group 0)
+//     then read back;  16: the same with wait_group.read only (no write wait)
 //  12-14: the roundtrip on an EXTRA CTA (grid + 1) that does no copy work:
 //  12 no fence, 13 fence.sc.sys after the stores (before the read back),
 //  14 fence.sc.sys after the read back
@@ -82,7 +84,30 @@ __global__ void __launch_bounds__(256) copyk(const int4* __restrict__ s, int4* _
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     return;
   }
-  if (blockIdx.x == 0 && threadIdx.x >= 32 && mode > 0) {
+  if ((mode == 15 || mode == 16) && blockIdx.x == 0 && threadIdx.x >= 32) {
+    __shared__ __align__(128) int4 sbuf[256];  // <= 4 KiB
+    const int t = threadIdx.x - 32, nt = blockDim.x - 32;
+    for (int i = t; i < hn16; i += nt) sbuf[i] = s[i];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory");
+    if (t == 0) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(host),
+                   "r"((unsigned)__cvta_generic_to_shared(sbuf)), "r"(hn16 * 16)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (mode == 15) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory");
+    if (mode == 15)
+      for (int i = t; i < hn16; i += nt) {
+        int4 v;
+        asm volatile("ld.global.cg.v4.s32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(host + i));
+        back[i] = v;
+      }
+  } else if (blockIdx.x == 0 && threadIdx.x >= 32 && mode > 0 && mode < 15) {
     const int t = threadIdx.x - 32, nt = blockDim.x - 32;
     for (int i = t; i < hn16; i += nt) st_mode(host + i, s[i], mode);
     if (mode == 5 || mode == 9) asm volatile("fence.sc.sys;" ::: "memory");
@@ -136,7 +161,7 @@ int main() {
   for (int rep = 0; rep < 2; ++rep)
     for (size_t bytes : sizes)
       for (int hb : {512, 4096})
-        for (int mode : {0, 1, 5, 7, 9, 10, 12, 13, 14}) {
+        for (int mode : {0, 1, 7, 10, 15, 16}) {
           cudaLaunchConfig_t lc = {};
           lc.gridDim = dim3(148 * 4 + (mode >= 12 ? 1 : 0));
           lc.blockDim = dim3(256);
