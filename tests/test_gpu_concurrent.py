@@ -143,3 +143,30 @@ def test_jacobi_ring_contention_free():
             d.zero_()
     assert eng.stats().kernels == 1  # every transfer's tiles in one kernel (loopback)
     eng.close()
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_programs_with_the_cross_device_lowering(graph):
+    """fault_inject & 2 (logical GPUs lowered as separate devices: system-
+    scope relay / host flags, host chunks as hop1 / hop2 tiles): a BIBW
+    pair through relays + host and a 4-ring halo exchange as ONE program
+    each, resent back to back, byte-exact."""
+    from paper_2604_22228_b200 import PathConfig
+    eng = _engine(4, fault_inject=2)
+    srcs, dsts, datas = _bufs([6 * MiB + 5, 6 * MiB + 9, 2 * MiB + 1, 2 * MiB + 3, 2 * MiB + 7, 2 * MiB + 11], 21)
+    bibw = eng.prepare_many([(srcs[0], dsts[0], None, 0, 1), (srcs[1], dsts[1], None, 1, 0)],
+                            PathConfig(num_gpu_paths=3, host_path_enabled=True, max_chunks=4, graph_mode=graph,
+                                       share_policy="equal"))
+    ring = eng.prepare_many([(srcs[2 + r], dsts[2 + r], None, r, (r + 1) % 4) for r in range(4)],
+                            PathConfig(num_gpu_paths=2, host_path_enabled=True, max_chunks=3, graph_mode=graph),
+                            joint=True)
+    for _ in range(3):
+        for d in dsts:
+            d.fill_(0)
+        bibw()
+        ring()
+        bibw()
+        eng.sync()
+        for d, want in zip(dsts, datas):
+            assert np.array_equal(d.cpu().numpy(), want)
+    eng.close()

@@ -130,3 +130,49 @@ def test_group_back_to_back_transfers(world, gpu_paths, host, graph):
     before the previous wait re-armed the counter, and the next wait timed
     out."""
     _dist_util.run(_b2b_worker, world, gpu_paths, host, graph)
+
+
+def _evict_worker(rank, world, port, graph):
+    import numpy as np
+    import torch.distributed as dist
+
+    import paper_2604_22228_b200 as mp
+    from oracle import transfer as ot
+    from paper_2604_22228_b200.group import TransferGroup
+    _dist_util.init(rank, world, port)
+    torch.cuda.set_device(0)
+    topo = mp.load_topology(mp.mesh_text("g", world, 7.5e11, 1, 2e-6, 5.5e10, 1e-5, "full"))
+    grp = TransferGroup(topo, device=0, stage_bytes=64 << 20)
+    sizes = [(3 << 20) + 5, (5 << 20) + 9]
+    pairs = []
+    for i, n in enumerate(sizes):
+        s = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+        d = torch.empty(n, dtype=torch.uint8, device="cuda:0")
+        if rank == 0:
+            s.copy_(torch.from_numpy(ot.pattern(n, seed=60 + i)))
+        pairs.append((grp.expose(s, owner=0), grp.expose(d, owner=1), d, n))
+    torch.cuda.synchronize()
+    dist.barrier()
+    cfg = mp.PathConfig(num_gpu_paths=world - 1, host_path_enabled=True, max_chunks=3, graph_mode=graph,
+                        cache_capacity=1)
+    stream = torch.cuda.Stream(device=0)
+    for _ in range(3):  # alternating pairs with capacity 1: every transfer evicts the other entry
+        for sb, db, _, n in pairs:
+            grp.transfer(sb, db, n, cfg, stream=stream)
+    stream.synchronize()
+    grp.sync()
+    if rank == 1:
+        for i, (_, _, d, n) in enumerate(pairs):
+            assert np.array_equal(d.cpu().numpy(), ot.pattern(n, seed=60 + i))
+    dist.barrier()
+    grp.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("graph", [False, True])
+def test_group_back_to_back_with_cache_eviction(world, graph):
+    """cache_capacity 1 and two alternating buffer pairs, back to back with
+    no host sync: every transfer evicts (and syncs on) the other entry while
+    the peers' kernels are in flight — byte-exact, no timeout."""
+    _dist_util.run(_evict_worker, world, graph)
