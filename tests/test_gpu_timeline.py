@@ -41,18 +41,30 @@ def _ordering_ok(plan, tl):
             assert slot["stage_hop2"].start_time >= slot["stage_hop1"].end_time
 
 
-@pytest.mark.parametrize("relay,host", [("sm", "ce"), ("ce", "ce"), ("sm", "sm")])
-def test_trace_is_a_valid_timeline(relay, host):
+@pytest.mark.parametrize("relay,host,fault", [("sm", "ce", 0), ("ce", "ce", 0), ("sm", "sm", 0), ("sm", "sm", 2)])
+def test_trace_is_a_valid_timeline(relay, host, fault):
+    """fault = 2: the cross-device lowering (system-scope flags, host chunks
+    as hop1 / hop2 tiles) traced between cached sends of the same buffers."""
     from paper_2604_22228_b200 import PathConfig
-    eng, text = _engine(4, relay=relay, host=host)
+    eng, text = _engine(4, relay=relay, host=host, fault_inject=fault)
     size = 16 * MiB + 777
     cfg = PathConfig(num_gpu_paths=3, host_path_enabled=True, max_chunks=4, share_policy="equal")
     data = ot.pattern(size, seed=11)
     src = torch.from_numpy(data).to("cuda:0")
     dst = torch.bitwise_not(src)
+    if fault:  # cached graph sends around the traced one
+        for _ in range(2):
+            eng.send(src, dst, size, PathConfig(3, True, 4, True, share_policy="equal"), src_dev=0, dst_dev=1)
+        eng.sync()
+        dst.copy_(torch.bitwise_not(src))
     plan, tl = eng.trace(src, dst, size, cfg, src_dev=0, dst_dev=1)
     eng.sync()
     assert np.array_equal(dst.cpu().numpy(), data)
+    if fault:
+        dst.zero_()
+        eng.send(src, dst, size, PathConfig(3, True, 4, True, share_policy="equal"), src_dev=0, dst_dev=1)
+        eng.sync()
+        assert np.array_equal(dst.cpu().numpy(), data)
     # plan == oracle, one task per logical node, sane times
     paths = op.plan_paths(op.parse_topology(text), 0, 1, 3, True, "equal")
     assert [(c.path_index, c.offset, c.length, c.seq) for c in plan.chunks] == \
