@@ -56,6 +56,8 @@ def test_timed_out_wait_is_sticky_and_never_copies_staging(kind):
         eng.send(src, dst, size, cfg, src_dev=0, dst_dev=1)
     with pytest.raises(EngineError, match="timed out"):
         eng.recv(dst)
+    with pytest.raises(EngineError, match="timed out"):  # programs too (mp_send_many)
+        eng.send_many([(src, dst, size, 0, 1)], cfg)
     got = dst.cpu().numpy()
     staged = [c for c in chunks if paths[c[0]]["kind"] != "direct"]
     muted = staged[0]
