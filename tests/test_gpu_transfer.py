@@ -465,3 +465,29 @@ def test_eviction_under_multi_stream_churn():
     for src, dst, n, data in pairs:
         assert np.array_equal(dst.cpu().numpy(), data), f"{n} B"
     eng.close()
+
+
+def test_no_device_memory_leak_over_cache_churn_and_engine_cycles():
+    """300 distinct cached sends (capacity 4: constant eviction, graph
+    destroy) and 20 engine create / close cycles leave the device's free
+    memory where it was (tile tables, claim counters, arenas, graphs freed)."""
+    from paper_2604_22228_b200 import PathConfig
+    n = 256 * MiB  # dynamic tables of ~4k tiles (256 KiB each): a leak per entry shows
+    base = torch.empty(n + 4096, dtype=torch.uint8, device="cuda:0")
+    out = torch.empty_like(base)
+    torch.cuda.synchronize()
+
+    def free():
+        torch.cuda.synchronize()
+        return torch.cuda.mem_get_info(0)[0]
+    f0 = free()
+    for cycle in range(20):
+        eng, _ = _engine(3)
+        cfg = PathConfig(2, True, 3, True, cache_capacity=4)
+        for i in range(15 if cycle else 300):
+            off = (i * 16) % 4096
+            eng.send(base[off:off + n], out[off:off + n], n, cfg, src_dev=0, dst_dev=1)
+        eng.sync()
+        eng.close()
+    f1 = free()
+    assert f0 - f1 < 16 * MiB, f"device memory dropped by {(f0 - f1) / MiB:.1f} MiB"
