@@ -49,6 +49,8 @@ enum ProgKind { PROG_DYNAMIC = 0, PROG_STATIC_TMA = 1, PROG_SMALL = 2 };
 constexpr uint64_t kPdlMinBytes = 1 << 20;
 constexpr int kPeerCtasPerSm = 4;
 constexpr uint64_t kVecTileBytes = 64 << 10;
+// ... and of GPU-relay hops on it (lowering.cuh lower_relay)
+constexpr uint64_t kRelayTileBytes = 128 << 10;
 bool tma_ok(const mp_engine_opts& o, bool peer) {
   return !(o.tma_peer < 0 || (peer && o.tma_peer == 0));
 }

@@ -495,8 +495,19 @@ class Lowering {
                             n_b});
       return;
     }
-    const uint64_t t1 = tile_for(sp, pi.bytes);
-    const uint64_t t2 = tile_for(rp, pi.bytes);  // 64 KiB on the LDG/STG kernel (+4% vs auto)
+    // relay hops on the LDG/STG kernel: 128 KiB tiles (half the flag
+    // releases / acquires of the 64 KiB direct tiles) — 512 MiB through 1 / 2
+    // / 6 relays +1-5% in loopback and +12-17% with system-scope flags (the
+    // cross-device lowering, fault_inject=2; tools/exp_relay_tiles.py)
+    uint64_t t1 = tile_for(sp, pi.bytes);
+    uint64_t t2 = tile_for(rp, pi.bytes);
+    if (o_.tile_bytes == 0 && t1 == kVecTileBytes && !static_tile_[sp]) t1 = kRelayTileBytes;
+    if (o_.tile_bytes == 0 && t2 == kVecTileBytes && !static_tile_[rp]) t2 = kRelayTileBytes;
+    if (const char* e = std::getenv("MP_RELAY_TILE")) {  // experiment knob
+      const uint64_t v = std::strtoull(e, nullptr, 10);
+      if (v && !static_tile_[sp]) t1 = v;
+      if (v && !static_tile_[rp]) t2 = v;
+    }
     // hop1 and hop2 on one device (loopback): release / acquire at GPU scope
     const uint32_t scope = same_gpu(sp, rp) ? mpk::TILE_SCOPE_GPU : 0u;
     mpk::Tile h1{};
