@@ -317,8 +317,11 @@ Entry* lookup_entry(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int 
 }
 
 
-// Group mode: tile size of relay hops, agreed by construction across ranks.
-constexpr uint64_t kGroupRelayTileBytes = 64 << 10;
+// Group mode: tile sizes of relay hops (128 KiB: half the system-scope flag
+// traffic, as kRelayTileBytes) and host hops (64 KiB: parallelism while the
+// PCIe path is the bottleneck), agreed by construction across ranks.
+constexpr uint64_t kGroupRelayTileBytes = 128 << 10;
+constexpr uint64_t kGroupHostTileBytes = 64 << 10;
 
 // Serialized CUDA-IPC handles of one rank's group resource block.
 struct GroupBlob {
@@ -388,7 +391,7 @@ Entry* build_group_entry(mp_ctx* ctx, const std::string& key, const void* src, u
       stage_off[p] += ch.length;
       const size_t cap = dr == me ? G->host_cap : G->peer_host_cap[dr];
       if (stage_off[p] > cap) throw Error{MP_ERR_STATE, "group host inbox too small for the host share"};
-      const uint64_t th = kGroupRelayTileBytes;
+      const uint64_t th = kGroupHostTileBytes;
       if (e->grole == 1) {
         uint8_t* slot = G->peer_host_dev[dr] + so;
         mpk::Tile h1{};
