@@ -708,6 +708,59 @@ def full_tables(torch, eng, text, dev, stream, size, pcie, hbm_peak) -> dict:
 _CPU_GROUP = None
 
 
+def nccl_single_process_p2p(torch, size: int, reps: int = 20, devs=(0, 1)) -> float:
+    """Baseline only: ncclCommInitAll over GPUs `devs` in THIS
+    process and ncclSend(GPU0) / ncclRecv(GPU1) of `size` bytes in a group,
+    `reps` back to back; GB/s from CUDA events on both devices' streams
+    (max).  Binds the NCCL library torch loaded (ctypes; no product code)."""
+    import ctypes as C
+    nccl = C.CDLL("libnccl.so.2")
+    nccl.ncclGetErrorString.restype = C.c_char_p
+    nccl.ncclGetErrorString.argtypes = [C.c_int]
+    nccl.ncclCommInitAll.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+    p2p = [C.c_void_p, C.c_size_t, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+    nccl.ncclSend.argtypes = p2p
+    nccl.ncclRecv.argtypes = p2p
+    nccl.ncclCommDestroy.argtypes = [C.c_void_p]
+
+    def ok(rc):
+        if rc != 0:
+            raise RuntimeError("NCCL: " + nccl.ncclGetErrorString(rc).decode())
+    n = len(devs)
+    comms = (C.c_void_p * n)()
+    ok(nccl.ncclCommInitAll(comms, n, (C.c_int * n)(*devs)))
+    try:
+        bufs = [torch.randint(0, 256, (size,), dtype=torch.uint8, device=f"cuda:{devs[0]}"),
+                torch.empty(size, dtype=torch.uint8, device=f"cuda:{devs[1]}")]
+        streams = [torch.cuda.Stream(device=d) for d in devs]
+        uint8, cnt = 1, C.c_size_t(size)  # ncclUint8
+
+        def step():
+            ok(nccl.ncclGroupStart())
+            ok(nccl.ncclSend(bufs[0].data_ptr(), cnt, uint8, 1, comms[0], streams[0].cuda_stream))
+            ok(nccl.ncclRecv(bufs[1].data_ptr(), cnt, uint8, 0, comms[1], streams[1].cuda_stream))
+            ok(nccl.ncclGroupEnd())
+        for _ in range(3):
+            step()
+        for d in devs:
+            torch.cuda.synchronize(d)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in devs]
+        for (e0, _), s_ in zip(ev, streams):
+            e0.record(s_)
+        for _ in range(reps):
+            step()
+        for (_, e1), s_ in zip(ev, streams):
+            e1.record(s_)
+        for d in devs:
+            torch.cuda.synchronize(d)
+        assert torch.equal(bufs[0].cpu(), bufs[1].cpu()), "NCCL p2p bytes differ"
+        ms = max(e0.elapsed_time(e1) for e0, e1 in ev)
+        return reps * size / (ms / 1e3) / 1e9
+    finally:
+        for c in comms:
+            nccl.ncclCommDestroy(c)
+
+
 def cpu_group():
     """A gloo group over every rank (host-side barriers and object gathers)."""
     global _CPU_GROUP
@@ -793,6 +846,8 @@ def run_node(args, rank: int, world: int) -> None:
             finally:
                 ce.close()
         t_ce = opt("peer_memcpy", ce_arm)
+        # baseline only: single-process NCCL (ncclCommInitAll) send/recv GPU0 -> GPU1
+        nccl_sp = opt("nccl_single_process", lambda: nccl_single_process_p2p(torch, size)) if ngpu >= 2 else None
         t_stream = opt("streamed", lambda: time_send(torch, eng, PathConfig(g, host, k, False), src, dst,
                                                      size, 20, stream))
         # roofline constituents measured on this box: per-path probe (direct
@@ -860,7 +915,7 @@ def run_node(args, rank: int, world: int) -> None:
             "path_roofline": {"R_gbs": R, "direct_probe_gbs": probe["direct_sm"], "ingress_gbs": ingress,
                               "egress_gbs": egress,
                               "pcie_probed_gbs": pcie, "single_path_sm_gbs": gbs(t_sm),
-                              "peer_memcpy_ce_gbs": gbs(t_ce),
+                              "peer_memcpy_ce_gbs": gbs(t_ce), "nccl_commInitAll_p2p_gbs": nccl_sp,
                               "multi_streamed_gbs": gbs(t_stream), "relay_sweep": relays},
             "e2e": ({"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": size, "d2h_bytes_per_step": 8}
                     if e2e else {"unavailable": errors.get("e2e", "")}),

@@ -5,6 +5,9 @@ oracle, with the plan equal to the oracle's.  Also the TMA bulk-copy kernel
 on peer addresses (`tma_peer`), which the 1-GPU pool cannot verify.
 On one GPU every one of these paths runs in loopback in test_gpu_transfer.py."""
 
+import os
+import sys
+
 import numpy as np
 import pytest
 
@@ -157,3 +160,12 @@ def test_egress_probe_one_gpu_to_all_peers():
     for s, t, _ in bufs:
         assert torch.equal(s.cpu(), t.cpu())
     eng.close()
+
+
+@needs2
+def test_nccl_single_process_baseline():
+    """The bench's baseline-only ncclCommInitAll + ncclSend/Recv GPU0 -> GPU1
+    (one process) delivers the bytes and reports a rate."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    assert bench.nccl_single_process_p2p(torch, 64 * MiB + 3, reps=5) > 0
