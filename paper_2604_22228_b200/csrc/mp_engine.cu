@@ -558,6 +558,24 @@ void remember_plan(mp_ctx* ctx, const Entry* e) {
   ctx->last_plan_epoch = ctx->cache_epoch;
 }
 
+// A send enqueued into a CUDA stream capture (the caller building its own
+// graph): the cached program is recorded as nodes of that graph (enqueue,
+// never a nested cudaGraphLaunch), no engine event is recorded or waited on
+// (an event recorded inside a capture is unusable outside it — it broke
+// every later cross-stream send), and a cache miss is refused (building a
+// program allocates and uploads, which a capture forbids).
+bool stream_capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs != cudaStreamCaptureStatusNone;
+}
+
+const char* const kCaptureMiss =
+    "a send inside a CUDA stream capture must hit the plan cache: send it once outside the capture first";
+
 uint64_t timeout_ns(const mp_engine_opts& o) { return (uint64_t)o.wait_timeout_ms * 1000000ull; }
 
 // (Re)initialise a device's control block: zero counters and error word,
@@ -829,6 +847,7 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
   cudaStream_t user = (cudaStream_t)stream;
+  const bool capturing = stream_capturing(user);
   // resend of the last single send (back-to-back messages on one buffer
   // pair): the same key bytes and its entry still cached — a hit without
   // the hash lookup (the key buffer is reused: a hit allocates nothing)
@@ -845,6 +864,7 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
     hs.cache_hits++;
     hs.creation_us = hs.construction_us = hs.instantiation_us = hs.plan_us = 0.0;
   } else {
+    if (capturing && ctx->index.find(key) == ctx->index.end()) throw Error{MP_ERR_STATE, kCaptureMiss};
     e = lookup_entry(ctx, src, dst, size, src_dev, dst_dev, *cfg, user, nullptr, &key);
     lo.key = key;
     lo.entry = e;
@@ -855,19 +875,22 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
   Phys& S = ctx->phys[e->src_phys];
   set_device(S.ordinal);
   // serialise with a send issued on another stream (shared counters/arenas)
-  if (ctx->have_last && ctx->last_stream != stream) CK(cudaStreamWaitEvent(user, ctx->last_done, 0));
+  if (!capturing && ctx->have_last && ctx->last_stream != stream)
+    CK(cudaStreamWaitEvent(user, ctx->last_done, 0));
   double t_launch = now_us();
-  bool timing = !cfg->graph_mode && ctx->kernel_timing;
-  if (cfg->graph_mode && e->graph && !pdl_replay(ctx, e)) {
+  bool timing = !cfg->graph_mode && ctx->kernel_timing && !capturing;
+  if (cfg->graph_mode && e->graph && !pdl_replay(ctx, e) && !capturing) {
     CK(cudaGraphLaunch(e->exec, user));
     st.ce_copies = (int)e->ce.size();
   } else {
     enqueue(ctx, e, user, timing);
     st.ce_copies = (int)e->ce.size();
   }
-  CK(cudaEventRecord(ctx->last_done, user));
-  ctx->have_last = true;
-  ctx->last_stream = stream;
+  if (!capturing) {
+    CK(cudaEventRecord(ctx->last_done, user));
+    ctx->have_last = true;
+    ctx->last_stream = stream;
+  }
   st.launch_us = now_us() - t_launch;
   st.graph_mode = cfg->graph_mode ? 1 : 0;
   st.nodes_logical = e->nodes_logical;
@@ -891,6 +914,7 @@ int mp_send_many(mp_ctx* ctx, const mp_xfer* xfers, int32_t n, const mp_config* 
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
   cudaStream_t user = (cudaStream_t)stream;
+  const bool capturing = stream_capturing(user);  // see mp_send
   auto& lm = ctx->last_many;
   Entry* e = nullptr;
   if (lm.entry && lm.epoch == ctx->cache_epoch && lm.joint == joint && (int)lm.xfers.size() == n &&
@@ -921,6 +945,7 @@ int mp_send_many(mp_ctx* ctx, const mp_xfer* xfers, int32_t n, const mp_config* 
     }
   }
   if (!e) {
+    if (capturing && ctx->index.find(key) == ctx->index.end()) throw Error{MP_ERR_STATE, kCaptureMiss};
     e = lookup_entry(
       ctx, xfers[0].src, xfers[0].dst, xfers[0].size, xfers[0].src_dev, xfers[0].dst_dev, *cfg, user,
       [&](const std::string& k) {
@@ -946,14 +971,17 @@ int mp_send_many(mp_ctx* ctx, const mp_xfer* xfers, int32_t n, const mp_config* 
   }
   mp_send_stats& st = ctx->stats;
   Phys& S = ctx->phys[e->src_phys];
-  CK(cudaSetDevice(S.ordinal));
-  if (ctx->have_last && ctx->last_stream != stream) CK(cudaStreamWaitEvent(user, ctx->last_done, 0));
+  set_device(S.ordinal);
+  if (!capturing && ctx->have_last && ctx->last_stream != stream)
+    CK(cudaStreamWaitEvent(user, ctx->last_done, 0));
   double t0 = now_us();
-  if (cfg->graph_mode && e->graph) CK(cudaGraphLaunch(e->exec, user));
+  if (cfg->graph_mode && e->graph && !capturing) CK(cudaGraphLaunch(e->exec, user));
   else enqueue(ctx, e, user, false);
-  CK(cudaEventRecord(ctx->last_done, user));
-  ctx->have_last = true;
-  ctx->last_stream = stream;
+  if (!capturing) {
+    CK(cudaEventRecord(ctx->last_done, user));
+    ctx->have_last = true;
+    ctx->last_stream = stream;
+  }
   st.launch_us = now_us() - t0;
   st.graph_mode = cfg->graph_mode ? 1 : 0;
   st.nodes_logical = e->nodes_logical;
