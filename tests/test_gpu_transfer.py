@@ -491,3 +491,23 @@ def test_no_device_memory_leak_over_cache_churn_and_engine_cycles():
         eng.close()
     f1 = free()
     assert f0 - f1 < 16 * MiB, f"device memory dropped by {(f0 - f1) / MiB:.1f} MiB"
+
+
+def test_default_usage_on_the_current_stream_with_typed_tensors():
+    """The minimal call a user writes: eng.send(src, dst) with float tensors,
+    no config (PathConfig.from_env), no stream (the current stream), no
+    devices (from the tensors), then eng.recv(dst) on the current stream."""
+    from paper_2604_22228_b200 import Engine, PathConfig
+    eng = Engine.loopback(2)
+    src = torch.randn(3 * MiB + 5, device="cuda:0")
+    dst = torch.zeros_like(src)
+    eng.send(src, dst)
+    eng.recv(dst)
+    assert torch.equal(src, dst)
+    # a multi-path config on the default stream, then a torch op that reads dst
+    src2 = torch.randn(8 * MiB + 3, dtype=torch.float64, device="cuda:0")
+    dst2 = torch.zeros_like(src2)
+    eng.send(src2, dst2, config=PathConfig(1, True, 4, True), src_dev=0, dst_dev=1)
+    eng.recv(dst2)
+    assert float((dst2 - src2).abs().max()) == 0.0
+    eng.close()
