@@ -1577,6 +1577,11 @@ int mp_group_send(mp_ctx* ctx, const void* src, uint32_t src_align, void* dst, u
   std::lock_guard<std::mutex> lk(ctx->mu);
   DeviceGuard g;
   cudaStream_t user = (cudaStream_t)stream;
+  // the device-side barrier counts transfers as they run; a captured
+  // transfer replayed out of step with the other ranks would desynchronise it
+  if (stream_capturing(user))
+    return fail(MP_ERR_STATE, "group transfers cannot be captured into a CUDA graph (the ranks' device barrier "
+                              "counts transfers as they run)");
   const void* ksrc = G->rank == src_rank ? src : nullptr;
   Entry* e = lookup_entry(ctx, ksrc, dst, size ^ ((uint64_t)src_align << 58), src_rank, dst_rank, *cfg,
                           user, [&](const std::string& key) {
