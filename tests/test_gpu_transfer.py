@@ -511,3 +511,30 @@ def test_default_usage_on_the_current_stream_with_typed_tensors():
     eng.recv(dst2)
     assert float((dst2 - src2).abs().max()) == 0.0
     eng.close()
+
+
+def test_two_engines_interleaved_on_shared_and_separate_streams():
+    """Two independent engines in one process (two libraries, say) sending
+    interleaved on one stream and on their own streams: separate control
+    blocks, arenas and caches — every delivery exact."""
+    from paper_2604_22228_b200 import PathConfig
+    a, _ = _engine(3)
+    b, _ = _engine(2)
+    shared, sa, sb = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    bufs = []
+    for i, n in enumerate([5 * MiB + 1, 7 * MiB + 3, 96 * MiB + 5, 2 * MiB]):
+        data = ot.pattern(n, seed=80 + i)
+        bufs.append((torch.from_numpy(data).to("cuda:0"), torch.zeros(n, dtype=torch.uint8, device="cuda:0"), n, data))
+    ca, cb = PathConfig(2, True, 4, True), PathConfig(1, True, 8, False)
+    for r in range(4):
+        for i, (src, dst, n, _) in enumerate(bufs):
+            eng, cfg = (a, ca) if (i + r) % 2 == 0 else (b, cb)
+            stream = shared if r % 2 == 0 else (sa if eng is a else sb)
+            eng.send(src, dst, n, cfg, stream=stream, src_dev=0, dst_dev=1)
+    torch.cuda.synchronize()
+    a.sync()
+    b.sync()
+    for src, dst, n, data in bufs:
+        assert np.array_equal(dst.cpu().numpy(), data), n
+    a.close()
+    b.close()
