@@ -101,6 +101,10 @@ class TransferGroup:
         dist.barrier(group=group)
 
     def close(self):
+        """Free this rank's resources.  Peers' kernels write into this rank's
+        memory (staging, flags, host inbox, exposed buffers), so close every
+        rank only after the last transfer finished everywhere — `sync()` on
+        each rank, then a barrier (as the tests do)."""
         if getattr(self, "_ctx", None):
             lib.mp_ctx_destroy(self._ctx)
             self._ctx = None
