@@ -258,6 +258,11 @@ struct Entry {
   bool graph = false;
   int grole = 0;                  // group mode: 0 none, 1 sender, 2 relay, 3 receiver
   unsigned long long expected = 0;  // group receiver: bytes that must land
+  // recorded into a caller's CUDA graph (a send inside a stream capture):
+  // that graph's nodes point at this entry's tile tables, so LRU eviction
+  // skips it (clear_cache / set_topology / arena growth / close still free
+  // it, and with it the validity of those captured graphs)
+  bool pinned = false;
 };
 
 // Multi-process ("group") mode: one process per GPU.  Each rank owns a
@@ -395,6 +400,14 @@ void ensure_arenas(mp_ctx* ctx, const std::vector<size_t>& stage_need,
     if (stage_need[i] > ctx->logi[i].stage_cap || (flag_devs[i] && flags_need > ctx->logi[i].flag_cap))
       grow = true;
   if (!grow) return;
+  // growth frees the arenas every cached program points into; programs
+  // recorded into a caller's CUDA graph (pinned) would be left dangling in
+  // that graph, so refuse instead of corrupting a later replay
+  const auto pinned = std::count_if(ctx->lru.begin(), ctx->lru.end(), [](const Entry* x) { return x->pinned; });
+  if (pinned)
+    throw Error{MP_ERR_STATE, "this send needs larger staging arenas, which would free " + std::to_string(pinned) +
+                                  " program(s) captured into CUDA graphs: send the largest transfers once before "
+                                  "capturing, or clear_cache() and re-capture"};
   clear_cache(ctx);
   DeviceGuard g;
   for (size_t i = 0; i < ctx->logi.size(); ++i) {

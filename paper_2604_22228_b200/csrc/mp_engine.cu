@@ -300,8 +300,11 @@ Entry* lookup_entry(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int 
   ctx->lru.push_back(e);
   ctx->index[key] = std::prev(ctx->lru.end());
   while ((int)ctx->lru.size() > cfg.cache_capacity) {  // graph.py:184-185
-    Entry* old = ctx->lru.front();
-    ctx->lru.pop_front();
+    // the least recent entry not pinned by a caller's captured graph
+    auto victim = std::find_if(ctx->lru.begin(), ctx->lru.end(), [](const Entry* x) { return !x->pinned; });
+    if (victim == ctx->lru.end() || *victim == e) break;
+    Entry* old = *victim;
+    ctx->lru.erase(victim);
     ctx->index.erase(old->key);
     CK(cudaSetDevice(ctx->phys[old->src_phys].ordinal));
     // the old entry may still be replaying on `user` or on the stream of the
@@ -879,6 +882,7 @@ int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size, int32_t src_
     CK(cudaStreamWaitEvent(user, ctx->last_done, 0));
   double t_launch = now_us();
   bool timing = !cfg->graph_mode && ctx->kernel_timing && !capturing;
+  if (capturing) e->pinned = true;
   if (cfg->graph_mode && e->graph && !pdl_replay(ctx, e) && !capturing) {
     CK(cudaGraphLaunch(e->exec, user));
     st.ce_copies = (int)e->ce.size();
@@ -975,6 +979,7 @@ int mp_send_many(mp_ctx* ctx, const mp_xfer* xfers, int32_t n, const mp_config* 
   if (!capturing && ctx->have_last && ctx->last_stream != stream)
     CK(cudaStreamWaitEvent(user, ctx->last_done, 0));
   double t0 = now_us();
+  if (capturing) e->pinned = true;
   if (cfg->graph_mode && e->graph && !capturing) CK(cudaGraphLaunch(e->exec, user));
   else enqueue(ctx, e, user, false);
   if (!capturing) {

@@ -91,3 +91,42 @@ def test_a_miss_inside_a_capture_is_refused():
     eng.sync()
     assert torch.equal(src, dst)
     eng.close()
+
+
+def test_captured_programs_are_pinned_against_eviction_and_arena_growth():
+    """A captured program survives LRU eviction (its graph keeps replaying
+    exactly), and a send that would have to grow the staging arenas — which
+    would free the captured program's memory — is refused until clear_cache."""
+    from paper_2604_22228_b200 import Engine, EngineError, PathConfig, load_topology, mesh_text
+    eng = Engine(load_topology(mesh_text("pin", 3, 2e12, 1, 2e-6, 40e9, 1e-5, "full")), [0] * 3)
+    relay = PathConfig(2, True, 4, True, cache_capacity=2)
+    n = 4 * MiB + 3
+    src = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0")
+    dst = torch.zeros_like(src)
+    s = torch.cuda.Stream()
+    eng.send(src, dst, n, relay, stream=s, src_dev=0, dst_dev=1)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        eng.send(src, dst, n, relay, stream=s, src_dev=0, dst_dev=1)
+    # churn the LRU (capacity 2) with other small relay sends
+    others = [torch.randint(0, 256, (m,), dtype=torch.uint8, device="cuda:0") for m in (MiB, 2 * MiB, 3 * MiB)]
+    outs = [torch.zeros_like(o) for o in others]
+    for o, d in zip(others, outs):
+        eng.send(o, d, o.numel(), relay, stream=s, src_dev=0, dst_dev=1)
+    torch.cuda.synchronize()
+    assert eng.stats().cache_evictions >= 1
+    assert _replay_ok(g, [(src, dst)])
+    # a much larger relay share needs bigger arenas: refused while pinned
+    big = torch.randint(0, 256, (256 * MiB,), dtype=torch.uint8, device="cuda:0")
+    bout = torch.zeros_like(big)
+    with pytest.raises(EngineError, match="larger staging arenas"):
+        eng.send(big, bout, big.numel(), relay, stream=s, src_dev=0, dst_dev=1)
+    assert _replay_ok(g, [(src, dst)])  # still valid
+    del g
+    eng.clear_cache()  # the caller drops its graphs; now the arenas may grow
+    eng.send(big, bout, big.numel(), relay, stream=s, src_dev=0, dst_dev=1)
+    s.synchronize()
+    eng.sync()
+    assert torch.equal(big, bout)
+    eng.close()
