@@ -130,3 +130,26 @@ def test_captured_programs_are_pinned_against_eviction_and_arena_growth():
     eng.sync()
     assert torch.equal(big, bout)
     eng.close()
+
+
+@pytest.mark.parametrize("graph_mode", [True, False])
+def test_capture_of_a_program_with_copy_engine_lanes(graph_mode):
+    """host = "ce": the program forks onto the engine's lane streams (2-D
+    D2H / H2D copies) and joins back — inside a capture those streams join
+    the caller's graph; replays are byte-exact."""
+    from paper_2604_22228_b200 import Engine, PathConfig, load_topology, mesh_text
+    eng = Engine(load_topology(mesh_text("ce", 2, 2e12, 1, 2e-6, 50e9, 1e-5, "full")), [0, 0])
+    eng.configure(host="ce")
+    cfg = PathConfig(1, True, 8, graph_mode)
+    n = 96 * MiB + 5
+    src = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0")
+    dst = torch.zeros_like(src)
+    s = torch.cuda.Stream()
+    eng.send(src, dst, n, cfg, stream=s, src_dev=0, dst_dev=1)
+    s.synchronize()
+    assert eng.stats().ce_copies > 0
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        eng.send(src, dst, n, cfg, stream=s, src_dev=0, dst_dev=1)
+    assert _replay_ok(g, [(src, dst)])
+    eng.close()
