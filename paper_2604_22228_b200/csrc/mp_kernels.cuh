@@ -397,10 +397,12 @@ __device__ __forceinline__ void hop2_vectors(const uint8_t* s, uint8_t* d, uint6
 // fence is cheap here — and it retires the CTA's host writes early instead
 // of leaving them to the grid-completion flush, which queues behind any
 // saturating H2D DMA (an e2e window's 512 MiB upload: +20 us per 512 MiB
-// message, sends 11.5 -> 10.3 ms per window).  Dynamic tables (large
+// message, sends 11.5 -> 10.3 ms per window) and that a programmatic-
+// dependent next launch waits for (~0.7 us).  Dynamic tables (large
 // messages, roundtrips far off the critical path) fence; the static TMA
-// table's helper warps do not (at 4-16 MiB the roundtrip is the message's
-// tail and the fence measured +0.8-1.1 us).
+// table's helper warps fence when the tile carries TILE_FENCE (programs
+// from 20 MiB; below, the roundtrip is the message's tail and the fence
+// adds to it: 8 MiB 0.82 -> 0.65 of single path).
 template <int UNROLL>
 __device__ __forceinline__ void roundtrip(const Tile& t, unsigned tid, unsigned nt, unsigned bar,
                                           unsigned long long* trace, bool lead, bool fence) {
