@@ -176,3 +176,60 @@ def test_group_back_to_back_with_cache_eviction(world, graph):
     no host sync: every transfer evicts (and syncs on) the other entry while
     the peers' kernels are in flight — byte-exact, no timeout."""
     _dist_util.run(_evict_worker, world, graph)
+
+
+def _fuzz_worker(rank, world, port, ops, seed):
+    import random
+
+    import numpy as np
+    import torch.distributed as dist
+
+    import paper_2604_22228_b200 as mp
+    from oracle import transfer as ot
+    from paper_2604_22228_b200.group import TransferGroup
+    _dist_util.init(rank, world, port)
+    torch.cuda.set_device(0)
+    topo = mp.load_topology(mp.mesh_text("gf", world, 7.5e11, 1, 2e-6, 3e10, 1e-5, "full"))
+    grp = TransferGroup(topo, device=0, stage_bytes=96 << 20, host_bytes=96 << 20)
+    size = (6 << 20) + 77
+    mine = torch.from_numpy(ot.pattern(size, seed=900 + rank)).to("cuda:0")  # this rank's source
+    inbox = torch.zeros(size, dtype=torch.uint8, device="cuda:0")           # this rank's destination
+    srcs, dsts = [], []
+    for q in range(world):  # collective: every rank's source and destination, in rank order
+        srcs.append(grp.expose(mine, owner=q))
+        dsts.append(grp.expose(inbox, owner=q))
+    rng = random.Random(seed)  # the same sequence on every rank
+    stream = torch.cuda.Stream(device=0)
+    last_from = None  # who last wrote this rank's inbox (since the last check)
+    for step in range(ops):
+        a, b = rng.sample(range(world), 2)
+        n = rng.choice([1, 4097, (1 << 20) + 5, size])
+        cfg = mp.PathConfig(num_gpu_paths=rng.randint(1, world - 1), host_path_enabled=rng.random() < 0.5,
+                            max_chunks=rng.randint(1, 6), graph_mode=rng.random() < 0.7)
+        grp.transfer(srcs[a], dsts[b], n, cfg, stream=stream)
+        if rank == b:
+            last_from = (a, n)  # the last write into this inbox decides its first n bytes
+        if rng.random() < 0.15 or step == ops - 1:  # a check point (same decision on every rank)
+            stream.synchronize()
+            grp.sync()
+            dist.barrier()
+            if last_from is not None:
+                a_, n_ = last_from
+                got = inbox[:n_].cpu().numpy()
+                assert np.array_equal(got, ot.pattern(size, seed=900 + a_)[:n_]), (rank, step, last_from)
+            inbox.zero_()
+            torch.cuda.synchronize()
+            last_from = None
+            dist.barrier()
+    grp.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_group_random_transfer_sequences(world):
+    """Random back-to-back group transfers between random rank pairs (random
+    path counts, host path, chunking, graph / streamed), every rank taking
+    its part (sender, relay, receiver or idle) — receivers' inboxes checked
+    at random shared check points."""
+    _dist_util.run(_fuzz_worker, world, int(os.environ.get("MP_GROUP_FUZZ_OPS", "40")),
+                   int(os.environ.get("MP_GROUP_FUZZ_SEED", "7")))
