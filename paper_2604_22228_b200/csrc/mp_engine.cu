@@ -1114,6 +1114,10 @@ int mp_wait(mp_ctx* ctx, void* stream) {
   if (!ctx) return fail(MP_ERR_VALUE, "null argument");
   check_sticky(ctx);
   std::lock_guard<std::mutex> lk(ctx->mu);
+  // inside a caller's capture the sends recorded there are already ordered
+  // on the capturing stream, and waiting on the engine's (eager) event
+  // would break the capture: nothing to do
+  if (stream_capturing((cudaStream_t)stream)) return MP_OK;
   if (ctx->have_last) CK(cudaStreamWaitEvent((cudaStream_t)stream, ctx->last_done, 0));
   return MP_OK;
   GUARD_END

@@ -153,3 +153,34 @@ def test_capture_of_a_program_with_copy_engine_lanes(graph_mode):
         eng.send(src, dst, n, cfg, stream=s, src_dev=0, dst_dev=1)
     assert _replay_ok(g, [(src, dst)])
     eng.close()
+
+
+def test_send_recv_and_consumer_captured_together():
+    """The pattern send -> recv -> consumer, all recorded in one capture
+    after an eager send on another stream: recv inside the capture is a
+    no-op (the captured send is already ordered on the capture stream), the
+    capture stays valid, and replays deliver before the consumer reads."""
+    from paper_2604_22228_b200 import Engine, PathConfig
+    eng = Engine.loopback(2)
+    n = 32 * MiB + 1
+    cfg = PathConfig(1, True, 8, True)
+    src = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0")
+    dst = torch.zeros_like(src)
+    tail = torch.zeros(MiB, dtype=torch.uint8, device="cuda:0")
+    eng.send(src, dst, n, cfg, stream=torch.cuda.Stream(), src_dev=0, dst_dev=1)  # eager, other stream
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        eng.send(src, dst, n, cfg, stream=s, src_dev=0, dst_dev=1)
+        eng.recv(dst, stream=s)
+        tail.copy_(dst[-MiB:])
+    for _ in range(3):
+        src.random_(0, 256)
+        dst.zero_()
+        tail.zero_()
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(tail, src[-MiB:]) and torch.equal(src, dst)
+    eng.close()
