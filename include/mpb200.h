@@ -328,7 +328,9 @@ int mp_ctx_peer_matrix(const mp_ctx* ctx, int32_t* out, int32_t cap);
  * (key = src, dst, size, devices, path set; LRU of cudaGraphExec_t) or
  * per-call stream launch.  This is the B200 counterpart of the reference's
  * plan_paths -> make_chunk_plan -> graph_key -> GraphCache.get_or_build ->
- * simulate_graph chain (sim.py:272-277). */
+ * simulate_graph chain (sim.py:272-277).  On a stream being captured into
+ * the caller's CUDA graph, a cached program is recorded into that graph
+ * (and pinned against LRU eviction); a cache miss fails with MP_ERR_STATE. */
 int mp_send(mp_ctx* ctx, const void* src, void* dst, uint64_t size,
             int32_t src_dev, int32_t dst_dev, const mp_config* cfg, void* stream);
 /* One transfer of a concurrent batch. */
