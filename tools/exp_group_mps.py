@@ -38,10 +38,11 @@ def main():
     rows = []
     for host_bw in [0.0] + [float(x) * 1e9 for x in os.environ.get("HOST_BWS", "10,20,40").split(",")]:
         topo = mp.load_topology(mp.mesh_text("g", world, link, 1, 2e-6, host_bw or 1e9, 1e-5, "full"))
-        grp = TransferGroup(topo, device=0, stage_bytes=64 << 20, host_bytes=128 << 20)
+        grp = TransferGroup(topo, device=0, stage_bytes=512 << 20, host_bytes=128 << 20)
         sb = grp.expose(src, owner=0)
         db = grp.expose(dst, owner=1)
-        cfg = mp.PathConfig(num_gpu_paths=1, host_path_enabled=host_bw > 0, max_chunks=8,
+        gp = int(os.environ.get("GPU_PATHS", "1"))  # 1 + relay ranks (<= world - 1)
+        cfg = mp.PathConfig(num_gpu_paths=gp, host_path_enabled=host_bw > 0, max_chunks=8,
                             graph_mode=os.environ.get("GRAPH", "1") == "1")
         stream = torch.cuda.Stream(device=0)
         dst.zero_()
@@ -70,8 +71,9 @@ def main():
         grp.sync()
         if rank == 0:
             paths, chunks = grp.last_plan()
-            host_bytes = sum(c.length for c in chunks if c.path_index == 1)
-            rows.append({"world": world, "host_plan_gbs": host_bw / 1e9, "host_share": round(host_bytes / size, 4),
+            kinds = [pth.kind for pth in paths]
+            host_bytes = sum(c.length for c in chunks if kinds[c.path_index] == "host")
+            rows.append({"world": world, "gpu_paths": gp, "host_plan_gbs": host_bw / 1e9, "host_share": round(host_bytes / size, 4),
                          "gbs": round(reps * size / (max(t) / 1e3) / 1e9, 1), "bytes_ok": oks[1]})
             print(json.dumps(rows[-1]), flush=True)
         grp.close()
