@@ -46,7 +46,14 @@ size_t kernel_smem(const mp_engine_opts& o) {
 enum ProgKind { PROG_DYNAMIC = 0, PROG_STATIC_TMA = 1, PROG_SMALL = 2 };
 // Small-message tables from this size launch with programmatic dependent
 // launch when opts.pdl is set (see pdl_replay in mp_engine.cu).
-constexpr uint64_t kPdlMinBytes = 1 << 20;
+constexpr uint64_t kPdlMinBytesDefault = 1 << 20;
+inline uint64_t pdl_min_bytes() {  // MP_PDL_MIN: experiments only
+  static const uint64_t v = [] {
+    const char* e = std::getenv("MP_PDL_MIN");
+    return e ? (uint64_t)std::strtoull(e, nullptr, 10) : kPdlMinBytesDefault;
+  }();
+  return v;
+}
 constexpr int kPeerCtasPerSm = 4;
 constexpr uint64_t kVecTileBytes = 64 << 10;
 // ... and of GPU-relay hops on it (lowering.cuh lower_relay)
@@ -100,7 +107,7 @@ void launch_transfer(const mp_engine_opts& o_in, unsigned grid, cudaStream_t s, 
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = attr;
-    lc.numAttrs = o_in.pdl && bytes >= kPdlMinBytes ? 1 : 0;
+    lc.numAttrs = o_in.pdl && bytes >= pdl_min_bytes() ? 1 : 0;
     if (ntiles <= mpk::kSmallTilesLo) {
       mpk::SmallTable<mpk::kSmallTilesLo> lo;
       std::copy(small->src, small->src + ntiles, lo.src);

@@ -129,7 +129,7 @@ bool pdl_replay(const mp_ctx* ctx, const Entry* e) {
       e->progs[0].phys != e->src_phys)
     return false;
   const Program& pr = e->progs[0];
-  if (pr.kind == PROG_SMALL) return pr.small && pr.bytes >= kPdlMinBytes;
+  if (pr.kind == PROG_SMALL) return pr.small && pr.bytes >= pdl_min_bytes();
   if (pr.kind == PROG_STATIC_TMA) return ctx->opts.pdl >= 2;
   return ctx->opts.pdl >= 3;  // dynamic tables: 128 MiB 45.8 -> 44.0 us, 512 MiB 162.4 -> 160.8 us
 }
