@@ -4,6 +4,10 @@ reference planner, independent of the C++ product.
 Inputs are plain values — a parsed topology dict and config fields — so the
 oracle shares no code with paper_2604_22228_b200.  Each function cites the
 reference code it restates (paths relative to /root/reference/pkg/src/mpsim).
+Parity pinned: tests/test_oracle.py checks it against tests/golden/*.json,
+which tests/golden/gen_golden.py produced by importing the reference itself
+(412 planner cases, LRU traces, parser cases); only tests/, smoke() and the
+bench's CPU-baseline / reference legs use it, never the product.
 """
 
 from __future__ import annotations
