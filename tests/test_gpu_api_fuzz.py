@@ -64,59 +64,81 @@ def test_random_api_sequences_stay_byte_exact():
         torch.cuda.synchronize()
 
     for step in range(ops):
-        op = rng.choices(["send", "many", "prepared", "recv", "capture", "replay", "trace", "clear", "check"],
-                         weights=[30, 8, 8, 6, 4, 6, 2, 2, 10])[0]
+        op = rng.choices(["send", "many", "prepared", "recv", "capture", "replay", "trace", "clear", "check",
+                          "configure", "topology"],
+                         weights=[30, 8, 8, 6, 4, 6, 2, 2, 10, 2, 1])[0]
         k = rng.randrange(len(pairs))
         c = rng.randrange(len(cfgs))
         s = rng.choice(streams)
         src, dst, n, _ = pairs[k]
         log.append((step, op, k, c))
-        if op == "send":
-            eng.send(src, dst, n, cfgs[c], stream=s, src_dev=0, dst_dev=1)
-            sent[k] = True
-        elif op == "many":
-            ks = rng.sample(range(len(pairs)), rng.randint(1, 4))
-            eng.send_many([(pairs[j][0], pairs[j][1], pairs[j][2], 0, 1) for j in ks], cfgs[c], stream=s)
-            for j in ks:
-                sent[j] = True
-        elif op == "prepared":
-            key = (k, c, streams.index(s))
-            if key not in prepared:
-                prepared[key] = eng.prepare(src, dst, n, cfgs[c], stream=s, src_dev=0, dst_dev=1)
-            prepared[key]()
-            sent[k] = True
-        elif op == "recv":
-            eng.recv(dst, stream=s)
-        elif op == "capture":
-            cs = torch.cuda.Stream()
-            for attempt in range(2):
+
+        def do():
+            if op == "send":
+                eng.send(src, dst, n, cfgs[c], stream=s, src_dev=0, dst_dev=1)
+                sent[k] = True
+            elif op == "many":
+                ks = rng.sample(range(len(pairs)), rng.randint(1, 4))
+                eng.send_many([(pairs[j][0], pairs[j][1], pairs[j][2], 0, 1) for j in ks], cfgs[c], stream=s)
+                for j in ks:
+                    sent[j] = True
+            elif op == "prepared":
+                key = (k, c, streams.index(s))
+                if key not in prepared:
+                    prepared[key] = eng.prepare(src, dst, n, cfgs[c], stream=s, src_dev=0, dst_dev=1)
+                prepared[key]()
+                sent[k] = True
+            elif op == "recv":
+                eng.recv(dst, stream=s)
+            elif op == "capture":
+                cs = torch.cuda.Stream()
+                for attempt in range(2):
+                    torch.cuda.synchronize()
+                    g = torch.cuda.CUDAGraph()
+                    try:
+                        with torch.cuda.graph(g, stream=cs):
+                            eng.send(src, dst, n, cfgs[c], stream=cs, src_dev=0, dst_dev=1)
+                    except EngineError as exc:  # evicted since (or never sent): refused, as documented
+                        assert "must hit the plan cache" in str(exc) and attempt == 0, exc
+                        eng.send(src, dst, n, cfgs[c], stream=s, src_dev=0, dst_dev=1)
+                        sent[k] = True
+                        continue
+                    graphs.append((g, k))
+                    break
+            elif op == "replay" and graphs:
+                g, gk = rng.choice(graphs)
+                torch.cuda.synchronize()  # a captured send is ordered by the caller
+                g.replay()
                 torch.cuda.synchronize()
-                g = torch.cuda.CUDAGraph()
-                try:
-                    with torch.cuda.graph(g, stream=cs):
-                        eng.send(src, dst, n, cfgs[c], stream=cs, src_dev=0, dst_dev=1)
-                except EngineError as exc:  # evicted since (or never sent): refused, as documented
-                    assert "must hit the plan cache" in str(exc) and attempt == 0, exc
-                    eng.send(src, dst, n, cfgs[c], stream=s, src_dev=0, dst_dev=1)
-                    sent[k] = True
-                    continue
-                graphs.append((g, k))
-                break
-        elif op == "replay" and graphs:
-            g, gk = rng.choice(graphs)
-            torch.cuda.synchronize()  # a captured send is ordered by the caller
-            g.replay()
-            torch.cuda.synchronize()
-            sent[gk] = True
-        elif op == "trace" and n >= 4096:
-            torch.cuda.synchronize()
-            eng.trace(src, dst, n, cfgs[c], 0, 1)
-            sent[k] = True
-        elif op == "clear":
-            graphs.clear()  # a captured graph points into the cached programs' tables
+                sent[gk] = True
+            elif op == "trace" and n >= 4096:
+                torch.cuda.synchronize()
+                eng.trace(src, dst, n, cfgs[c], 0, 1)
+                sent[k] = True
+            elif op == "clear":
+                graphs.clear()  # a captured graph points into the cached programs' tables
+                eng.clear_cache()
+                prepared.clear()
+            elif op == "check":
+                check_and_poison()
+            elif op in ("configure", "topology"):  # both drop the cache (and so captured graphs)
+                graphs.clear()
+                if op == "configure":
+                    eng.configure(host=rng.choice(["sm", "ce", "auto"]), pdl=rng.randint(0, 3),
+                                  copy=rng.choice(["tma", "vec"]), sched=rng.choice(["auto", "dynamic"]))
+                else:
+                    eng.set_topology(load_topology(mesh_text("fz", 4, rng.choice([2e12, 7.5e11]), 1, 2e-6,
+                                                             rng.choice([1e9, 30e9, 55e9]), 1e-5, "full")))
+
+        try:
+            do()
+        except EngineError as exc:
+            # documented remedy: a send that must grow the staging arenas is
+            # refused while captured programs exist — drop the graphs, clear
+            # the cache, retry
+            assert "larger staging arenas" in str(exc), exc
+            graphs.clear()
             eng.clear_cache()
-            prepared.clear()
-        elif op == "check":
-            check_and_poison()
+            do()
     check_and_poison()
     eng.close()
