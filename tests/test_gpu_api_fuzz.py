@@ -1,8 +1,9 @@
 """Randomised API-level soak: random sequences of the calls a user makes —
 send (graph / streamed, several path configs), send_many windows, prepared
 sends, recv on another stream, sends captured into the caller's own CUDA
-graph and replayed, traced sends, cache clears, syncs — on several streams
-of one engine, with every buffer pair's destination checked byte-exact at
+graph and replayed, traced sends, cache clears, engine reconfiguration
+(host engine, PDL level, copy kernel, schedule) and topology changes, syncs
+— on several streams of one engine, with every buffer pair's destination checked byte-exact at
 each sync point (destinations are re-poisoned after each check, so a stale
 or missing delivery shows).  MP_API_FUZZ_OPS sets the length (default 120;
 a 2000-op soak is in profiles/)."""
