@@ -247,7 +247,7 @@ def run_reference(args, rank: int, world: int) -> None:
               f"{planner}, oracle/transfer.py numpy copies on {threads} threads")
     emit({"impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": world,
           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-          "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+          "higher_is_better": True, "scaling": "strong",
           "vs_baseline": None, "dtype": "u8", "data": "synthetic", "config": workload_config(args, world),
           "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
                            "sample": sample, **cpu_info()},
@@ -575,7 +575,7 @@ def run_one(args) -> None:
     out = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (seeded random bytes, seed 20261017)", "config": workload_config(args, 1),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": ncu_traffic(),
