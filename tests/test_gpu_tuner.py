@@ -118,3 +118,25 @@ def test_tune_rejects_an_infeasible_grid():
     with pytest.raises(ValueError, match="feasible"):
         tune(eng, [MiB], [GridPoint(3, False, 1)], modes=("graph",), reps=2)
     eng.close()
+
+
+def test_probe_topology_plans_and_sends():
+    """Engine.probe_topology writes a reference-schema .topo from measured
+    rates (the direct link and the host-staged path's delivered rate), which
+    the planner parses back and the engine sends with, byte-exact."""
+    import paper_2604_22228_b200 as mp
+    from paper_2604_22228_b200 import PathConfig
+    eng = _engine(2)
+    text = eng.probe_topology(64 * MiB, 3, name="probed2")
+    link, host = eng.probe_bandwidths(64 * MiB, 3)
+    assert link > 1e11 and 1e9 < host < 1e11
+    topo = mp.load_topology(text)
+    assert topo.name == "probed2" and len(topo.accelerators) == 2
+    eng.set_topology(topo)
+    n = 24 * MiB + 5
+    src = torch.randint(0, 256, (n,), dtype=torch.uint8, device="cuda:0")
+    dst = torch.bitwise_not(src)
+    eng.send(src, dst, n, PathConfig(1, True, 8, True), src_dev=0, dst_dev=1)
+    eng.sync()
+    assert torch.equal(src, dst)
+    eng.close()
